@@ -1,0 +1,404 @@
+"""Benchmark: (pair, knob) configs evaluated per second on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
+
+A step is one full build_graph sweep of the workload with inputs resident in
+HBM: per-app/per-knob tables -> solo splits -> fused pair x knob sweep ->
+exact re-scan of near-ties -> symmetric N x N weight scatter, replayed as one
+CUDA graph.  L2 is flushed (256 MiB memset) before every step, outside the
+events.  `value` = reference-equivalent (pair, config) evaluations (P x sum of
+per-budget configs) / sum of the per-step CUDA-event times, max over ranks.
+
+`e2e` = the same metric through the host-buffer C ABI (cs_build_graph_host):
+pinned host features in, H2D, the five kernels, D2H of the N x N weights and
+the per-pair records, all inside the timed region (wall clock; the call
+synchronizes).  `roofline` = the dominant kernel (k_sweep), its algorithmic
+flops (1,368 per unit: layer 2 + head for both members after the exact layer-1
+factorization) over its own event-timed duration against the
+measured dense bf16 tensor peak.  `cpu_baseline` / `--impl reference` = the
+oracle port (oracle/cosched_oracle.c, factored fp64, all host threads) on a
+bounded sample of the same workload.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): weak scaling -- the app count
+grows with sqrt(N) so every GPU sweeps the same number of pairs; each rank
+sweeps its contiguous pair shard, then one NCCL all-gather of the records and
+a device scatter build the full matrix on every rank.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_UNIT = 1368          # 2 members x 2 x (18*18 + 18) MAC-flops, SURVEY.md §8d
+
+WORKLOADS = {
+    # name: (n_apps, budgets (p_total, cap_sum_levels), cap grid, description)
+    "paper20": (20, [(400.0, (350, 400))], "default",
+                "paper-scale: 20 apps x full knob grid (100 co-run configs @ 400 W)"),
+    "n256": (256, [(400.0, (350, 400))], "default",
+             "256 apps (32,640 pairs) x full knob grid (100 co-run configs @ 400 W) on 1 B200"),
+    "n1024x5": (1024, [(p, (300, 325, 350, 375, 400)) for p in (300.0, 325.0, 350.0, 375.0, 400.0)],
+                "default", "1,024 apps x full knob grid, sweep of 5 total-power budgets"),
+    "n4096": (4096, [(400.0, (350, 400))], "default",
+              "4,096 apps (8.4M pairs) x full knob grid (100 configs @ 400 W)"),
+    "n4096fine": (4096, [(400.0, (350, 400))], "fine",
+                  "4,096 apps x fine cap grid (6.25 W steps, 340 configs @ 400 W)"),
+}
+FINE_CPU = tuple(100.0 + 6.25 * k for k in range(25))
+FINE_GPU = tuple(150.0 + 6.25 * k for k in range(17))
+
+
+def spaces_for(name):
+    from paper_2405_03831_b200 import core
+    n, budgets, grid, _ = WORKLOADS[name]
+    kw = {"cpu_caps": FINE_CPU, "gpu_caps": FINE_GPU} if grid == "fine" else {}
+    return n, [core.ConfigSpace(p_total=p, cap_sum_levels=lv, **kw) for p, lv in budgets]
+
+
+def load_weights():
+    from paper_2405_03831_b200 import fnn
+    return fnn.load_weights(os.path.join(ROOT, "tests", "golden", "weights.json"))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("bf16_tflops", 1590.0), d.get("hbm_gbs", 6650.0), "measured"
+    except (OSError, ValueError):
+        return 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+def cpu_baseline(weights, name, seconds=12.0, threads=None, n_override=None):
+    """Oracle port (factored fp64, threaded) on a bounded sample of the workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # checker / baseline only
+    from paper_2405_03831_b200 import synth
+    from paper_2405_03831_b200.grid import KnobGrid
+    n, spaces = spaces_for(name)
+    if n_override:
+        n = n_override
+    grid = KnobGrid(spaces)
+    F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
+    P = n * (n - 1) // 2
+    threads = threads or os.cpu_count() or 1
+    # sample: a contiguous pair range sized to ~1 s per pass, repeated for `seconds`
+    chunk = min(P, max(threads * 64, int(2.0e6 / max(1, grid.units_per_pair()) * threads / 8)))
+    oracle.sweep(weights, F, T, grid, 0, min(chunk, P), threads)  # warm
+    done, t0, passes = 0, time.perf_counter(), 0
+    while True:
+        b = (passes * chunk) % max(1, P - chunk + 1)
+        oracle.sweep(weights, F, T, grid, b, b + chunk, threads)
+        done += chunk
+        passes += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    units = done * grid.units_per_pair()
+    return {"value": units / dt, "unit": "configs/s", "cores": threads, "kind": "port",
+            "sample": f"{passes} passes x {chunk} pairs of the {n}-app workload "
+                      f"({grid.units_per_pair()} configs/pair) = {units:.3g} configs in {dt:.1f}s; "
+                      f"oracle/cosched_oracle.c factored fp64, {threads} threads"}
+
+
+def run_reference(args):
+    """The reference arm: the oracle port on all host cores, rank 0 only.
+
+    Each of the W + K steps is one bounded pass over a contiguous pair range of
+    the workload, sized from a calibration pass so the whole run takes ~90 s."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # baseline only
+    from paper_2405_03831_b200 import synth
+    from paper_2405_03831_b200.grid import KnobGrid
+    weights = load_weights()
+    n, spaces = spaces_for(args.workload)
+    grid = KnobGrid(spaces)
+    upp = grid.units_per_pair()
+    P = n * (n - 1) // 2
+    F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
+    threads = os.cpu_count() or 1
+    calib = min(P, threads * 256)
+    t0 = time.perf_counter()
+    oracle.sweep(weights, F, T, grid, 0, calib, threads)
+    rate = calib / max(time.perf_counter() - t0, 1e-6)          # pairs/s
+    budget = max(0.02, args.ref_budget_s / (args.steps + args.warmup))
+    chunk = int(min(P, max(threads * 16, rate * budget)))
+    vals, off = [], 0
+    for k in range(args.warmup + args.steps):
+        b = off % max(1, P - chunk + 1)
+        off += chunk
+        t0 = time.perf_counter()
+        oracle.sweep(weights, F, T, grid, b, b + chunk, threads)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            vals.append(chunk * upp / dt)
+    value = float(np.mean(vals))
+    sample = (f"{args.steps} timed passes x {chunk} contiguous pairs of the {n}-app workload "
+              f"({upp} configs/pair); oracle/cosched_oracle.c factored fp64 port, {threads} threads")
+    line = {"impl": "reference", "metric": "(pair,knob) configs evaluated/sec", "value": value,
+            "unit": "configs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": chunk * upp / value * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload][3], "n_apps": n, "pairs": P,
+                       "configs_per_pair": upp, "sample_pairs_per_step": chunk},
+            "cpu_baseline": {"value": value, "unit": "configs/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2405_03831_b200 import synth
+    from paper_2405_03831_b200.device import SweepPlan, to_device_inputs
+    from paper_2405_03831_b200.grid import KnobGrid
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    weights = load_weights()
+    n, spaces = spaces_for(args.workload)
+    if world > 1:   # weak scaling: pairs per GPU held at the 1-GPU count
+        n = int(round(n * math.sqrt(world) / 2.0)) * 2
+    grid = KnobGrid(spaces)
+    P = n * (n - 1) // 2
+    upp = grid.units_per_pair()
+    F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
+    d_f, d_b = to_device_inputs(F, T, dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    ev_s = torch.cuda.Event(enable_timing=True, external=True)
+    ev_e = torch.cuda.Event(enable_timing=True, external=True)
+    if world == 1:
+        plan = SweepPlan(weights, grid, n, device=dev, with_matrix=True)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                plan.launch(d_f, d_b)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            plan.launch(d_f, d_b, (ev_s, ev_e))
+        step = graph.replay
+        launches_per_step = plan.launches_per_run
+        units_local = P * upp
+    else:
+        from paper_2405_03831_b200.dist import ShardedSweep
+        sh = ShardedSweep(weights, grid, n, device=dev)
+        plan = sh.plan
+
+        def step():
+            sh.run(d_f, d_b, (ev_s, ev_e))
+        launches_per_step = 4 + grid.n_budgets
+        units_local = plan.P * upp
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    c = plan.read_counters()
+
+    # ---------------- timed region ----------------
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms, sweep_ms = [], []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local_rank) as clk:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()                       # L2 flush, outside the step events
+            st.record()
+            step()
+            en.record()
+            en.synchronize()
+            step_ms.append(st.elapsed_time(en))
+            sweep_ms.append(ev_s.elapsed_time(ev_e))
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(step_ms))
+    sweep_avg = float(np.mean(sweep_ms))
+    if world > 1:
+        t = torch.tensor([total_ms, sweep_avg], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, sweep_avg = float(t[0]), float(t[1])
+    value = P * upp * args.steps / (total_ms / 1e3)
+
+    result = None
+    if rank == 0:
+        tf, hbm, src = measured_peaks()
+        achieved_tflops = FLOPS_PER_UNIT * units_local / (sweep_avg / 1e3) / 1e12
+        result = {
+            "metric": "(pair,knob) configs evaluated/sec", "value": value, "unit": "configs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 screen / fp64 exact re-evaluation",
+            "data": "synthetic: simenv-equivalent workload (seed 0) + acceptance-recipe trained weights",
+            "config": {"workload": WORKLOADS[args.workload][3], "n_apps": n, "pairs": P,
+                       "configs_per_pair": upp, "budgets": [s.p_total for s in spaces],
+                       "l2": "flushed before every step (256 MiB memset, outside the events)",
+                       "step": "CUDA graph: tables, solo, sweep, resolve, scatter",
+                       "parallelism": f"pair shards x{world}"},
+            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tf,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / tf, "traffic": None,
+                         "kernel": "k_sweep", "kernel_ms": sweep_avg,
+                         "flops_per_unit": FLOPS_PER_UNIT, "units_per_launch": units_local,
+                         "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
+                         "kernel_share_of_step": sweep_avg / (total_ms / args.steps)},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "screen": {"queue_len": c.queue_len, "max_rel_gap": c.screen_error},
+            "wall_s_timed_region": wall,
+        }
+    # ---------------- e2e through the host-buffer C ABI (rank 0, 1 GPU) ----
+    if rank == 0 and not args.no_e2e:
+        from paper_2405_03831_b200.host_abi import HostGraphCall
+        from paper_2405_03831_b200 import matcher, scheduler
+        n1, sp1 = spaces_for(args.workload)
+        g1 = KnobGrid(sp1)
+        F1, T1 = synth.workload_arrays(0, synth.mixed_archetypes(n1))
+        call = HostGraphCall(weights, g1, n1, device=dev)
+        call.h_features[...] = F1
+        call.h_base_time[...] = T1
+        for _ in range(max(2, args.warmup)):
+            call()
+        k = max(3, min(args.steps, 200))
+        ts = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            call()
+            ts.append(time.perf_counter() - t0)
+        h2d, d2h = call.bytes_per_call()
+        P1 = n1 * (n1 - 1) // 2
+        e2e_val = P1 * g1.units_per_pair() / float(np.mean(ts))
+        result["e2e"] = {"value": e2e_val, "unit": "configs/s", "h2d_bytes_per_step": h2d,
+                         "d2h_bytes_per_step": d2h, "steps": k, "n_apps": n1,
+                         "api": "cs_build_graph_host (C ABI, pinned host buffers)"}
+        # second BASELINE metric: schedule time at this N (sweep + D2H + host matching)
+        jobs = synth.generate_workload(0, synth.mixed_archetypes(n1))
+        from paper_2405_03831_b200 import core as _core
+        inp = scheduler.SchedulerInput(tuple(jobs), sp1[-1], _core.SchedulingParams(window=n1),
+                                       weights)
+        if n1 <= 2048:
+            scheduler.schedule(inp)
+            t0 = time.perf_counter()
+            graph = scheduler.build_graph(inp)
+            t1 = time.perf_counter()
+            matched = matcher.min_weight_perfect_matching(graph)
+            t2 = time.perf_counter()
+            scheduler.emit_schedule(inp, graph, matched)
+            t3 = time.perf_counter()
+            result["schedule_e2e_s"] = {"total": t3 - t0, "build_graph": t1 - t0,
+                                        "matching": t2 - t1, "emit": t3 - t2, "n_apps": n1}
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        result["cpu_baseline"] = cpu_baseline(weights, args.workload, seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--workload", default="n256", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0,
+                    help="total wall budget of the --impl reference run")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

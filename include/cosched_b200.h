@@ -1,0 +1,183 @@
+/*
+ * cosched_b200.h -- C ABI of the B200 pair x knob sweep.
+ *
+ * The reference (arXiv 2405.03831, package `cosched`, pure Python) has no
+ * native boundary; the entry points below are what its optimizer/scheduler
+ * layer binds (ctypes stub in INTEGRATION.md) to replace, for a trained-FNN
+ * model, the per-pair Python loops:
+ *
+ *   cs_build_tables   replaces core.normalize_input (core.py:334-377) + the
+ *                     first layer of fnn.forward_batch (fnn.py:163) by factored
+ *                     per-app / per-knob partials computed once per sweep.
+ *   cs_solo           replaces estimator.solorun_time (estimator.py:139-180)
+ *                     via hwopt.optimize_solo_pair (hwopt.py:68-74), hoisted
+ *                     to one evaluation per (app, split).
+ *   cs_pair_sweep     replaces scheduler.build_graph's per-pair loop
+ *   + cs_resolve      (scheduler.py:52-78) over hwopt.decide_pair
+ *                     (hwopt.py:77-87) -> optimize_corun (hwopt.py:44-65) ->
+ *                     estimator.corun_time (estimator.py:112-129) ->
+ *                     slowdown floor (estimator.py:98-109).
+ *   cs_scatter_weights fills the symmetric N x N matrix handed to
+ *                     matcher.PairGraph (matcher.py:28-63; scheduler.py:73-77).
+ *   cs_forward_rows   replaces fnn.forward / forward_batch (fnn.py:146-165) for
+ *                     scalar queries (FnnSlowdownModel.predict_slowdown,
+ *                     estimator.py:59-67).
+ *   cs_build_graph_host  the whole build_graph with HOST buffers (H2D, tables,
+ *                     solo, sweep, resolve, scatter, D2H) in one call.
+ *
+ * Conventions: every `d_` pointer is device memory owned by the caller; every
+ * `h_` pointer is host memory (pinned for overlap, pageable works).  Nothing
+ * allocates; calls are stream-ordered on `stream` (a cudaStream_t, NULL =
+ * legacy default stream) and only cs_build_graph_host synchronizes.  No global
+ * mutable state: calls are re-entrant across host threads and devices.
+ * Return value: 0 on success, a negative CS_ERR_* code otherwise.
+ *
+ * Pairs are unordered (i < j) in row-major order, linear index
+ *   p(i, j) = i*(2N - i - 1)/2 + (j - i - 1)          (scheduler.py:61)
+ * and a shard is a contiguous range [pair_begin, pair_end).
+ */
+#ifndef COSCHED_B200_H
+#define COSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_NUM_FEATURES 18   /* core.py:18  */
+#define CS_INPUT_DIM 40      /* core.py:21  */
+#define CS_HIDDEN 18         /* fnn.py:19   */
+#define CS_MAX_BUDGETS 8     /* budgets swept in one call */
+
+enum {
+    CS_OK = 0,
+    CS_ERR_ARG = -1,          /* bad shape/size/pointer                -> ValidationError */
+    CS_ERR_NO_CONFIG = -2,    /* a budget admits no co-run config      (hwopt.py:62-64)   */
+    CS_ERR_UNREACHABLE = -3,  /* a budget admits no solo split         (estimator.py:165) */
+    CS_ERR_CUDA = -4,         /* CUDA launch/runtime failure           -> RuntimeError    */
+    CS_ERR_WORKSPACE = -5     /* workspace smaller than required       -> ValueError      */
+};
+
+/* NetworkWeights (fnn.py:42-68), HOST fp64, row-major exactly as the
+ * reference's JSON v1 document (fnn.py:311-324).  Copied by value into the
+ * kernel parameter bank at each launch. */
+typedef struct {
+    const double *w1;             /* 18 x 40 */
+    const double *b1;             /* 18      */
+    const double *w2;             /* 18 x 18 */
+    const double *b2;             /* 18      */
+    const double *w_out;          /* 1 x 18  */
+    const double *b_out;          /* 1       */
+    const double *feature_bounds; /* 36      */
+} cs_network;
+
+/* The knob grid of L budgets (core.py:380-407).  Configs are the union of
+ * each budget's co-run list, in the reference's lexicographic enumeration
+ * order (so first-index tie-breaking per budget is preserved).  knob rows are
+ * the normalized model inputs [cores/32, gpcs/8, cpu_cap/250, gpu_cap/250]
+ * (core.py:368-371) of the member-1 view and of the reversed-partition
+ * member-2 view (core.py:152-159).  mask[c] bit l = config c is legal in
+ * budget l.  Solo splits of budget l are rows [solo_offsets[l],
+ * solo_offsets[l+1]) of solo_knob ([1, 1, c/250, g/250]).
+ * Pointers are device memory for the device-level calls, host memory for
+ * cs_build_graph_host. */
+typedef struct {
+    int32_t n_grid;               /* G */
+    const double *knob1;          /* G x 4 */
+    const double *knob2;          /* G x 4 */
+    const uint32_t *mask;         /* G     */
+    int32_t n_budgets;            /* L, 1..CS_MAX_BUDGETS */
+    int32_t n_configs[CS_MAX_BUDGETS];         /* host: configs legal in budget l */
+    int32_t solo_offsets[CS_MAX_BUDGETS + 1];  /* host: solo rows of budget l */
+    const double *solo_knob;      /* solo_offsets[L] x 4 */
+} cs_grid;
+
+/* Device tables carved from one caller buffer by cs_tables_bind. */
+typedef struct {
+    int32_t n_apps, n_grid, n_solo;
+    double *net64;                /* fp64 copy of w2|b2|w_out|b_out for the exact path */
+    float *app_a32, *app_b32;     /* N x 20 (18 + pad): primary / co-runner partials */
+    double *app_a64, *app_b64;    /* N x 18 */
+    float *knob1_32, *knob2_32;   /* G x 20, b1 folded */
+    double *knob1_64, *knob2_64;  /* G x 18, b1 folded */
+    double *solo64;               /* S x 18, b1 folded */
+} cs_tables;
+
+/* Per-pair outputs of one shard, budget-major: element [l * P + (p - pair_begin)]. */
+typedef struct {
+    int32_t *corun_grid_index;    /* best config, index into the grid (-1: none) */
+    double *corun_time;           /* CoRunTime of that config, fp64 re-evaluated */
+    uint8_t *corun_chosen;        /* corun_time <= solo pair time (hwopt.py:86) */
+    double *weight;               /* winning_time (hwopt.py:39-41) */
+} cs_pair_out;
+
+/* Per-app solo results, budget-major [l * N + a]. */
+typedef struct {
+    double *solo_time;            /* best exclusive time at the budget */
+    int32_t *solo_split;          /* index within the budget's solo list */
+    int32_t *solo_clamps;         /* floor clamps over that app's splits */
+} cs_solo_out;
+
+const char *cs_version(void);
+const char *cs_error_string(int code);
+
+/* --- device-level, stream-ordered -------------------------------------- */
+size_t cs_tables_bytes(int32_t n_apps, int32_t n_grid, int32_t n_solo);
+int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, int32_t n_solo,
+                   cs_tables *out);
+
+int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
+                    const cs_grid *d_grid, const cs_tables *tables, void *stream);
+
+int cs_solo(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
+            cs_solo_out out, void *stream);
+
+/* `net` (host) is passed again because the fp32 screen keeps W2 in the kernel
+ * parameter bank.  Screens every (pair, config) of the shard in fp32, keeps per (pair, budget)
+ * the first-index minimum and the runner-up value; when the runner-up is more
+ * than `rel_eps` above the minimum the winner is re-evaluated in fp64 and the
+ * record finalized, otherwise the (pair, budget) is queued for cs_resolve,
+ * which re-scans it in fp64 (exact first-index argmin).  d_queue needs
+ * L * (pair_end - pair_begin) int64 slots.
+ * d_clamps (L x u64, zeroed by the caller) accumulates floor clamps exactly as
+ * the reference's clamp_stats counts them over build_graph (2 per co-run
+ * config + 2 x S solo per pair).  d_queue_count holds two zeroed u32: [0] the
+ * queue length, [1] the largest relative gap seen between an fp32-screened
+ * winner and its fp64 re-evaluation (float bits) -- a runtime check that the
+ * screen error stays far below rel_eps. */
+int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                  const double *d_base_time,
+                  const double *d_solo_time, const int32_t *d_solo_clamps, int64_t pair_begin,
+                  int64_t pair_end, double rel_eps, cs_pair_out out, int64_t *d_queue,
+                  uint32_t *d_queue_count, unsigned long long *d_clamps, void *stream);
+
+int cs_resolve(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
+               const double *d_solo_time, int64_t pair_begin, int64_t pair_end,
+               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+               void *stream);
+
+/* W[i*N+j] = W[j*N+i] = weight of budget `budget`; the caller zeroes W. */
+int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,
+                       int64_t pair_end, double *d_w, void *stream);
+
+/* fnn.forward_batch on rows x 40 normalized inputs (fp64, unfloored). */
+int cs_forward_rows(const cs_network *net, const double *d_x, int64_t rows, double *d_y,
+                    void *stream);
+
+/* --- host-buffer convenience: the whole build_graph --------------------- */
+size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid);
+/* h_weights: L x N x N (NULL to skip); h_pairs members: L x P host arrays
+ * (NULL members skipped); h_solo members: L x N host arrays (NULL skipped);
+ * h_clamps: L (NULL to skip).  Full graph (all P pairs). */
+int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
+                        const double *h_base_time, int32_t n_apps, double rel_eps,
+                        void *d_workspace, size_t workspace_bytes, double *h_weights,
+                        cs_pair_out h_pairs, cs_solo_out h_solo,
+                        unsigned long long *h_clamps, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COSCHED_B200_H */

@@ -1,0 +1,42 @@
+/*
+ * cosched_match.h -- host C ABI of the native matcher.
+ *
+ * Replaces the reference's pure-Python Edmonds blossom
+ * (matcher._max_weight_matching, matcher.py:180-542) behind
+ * matcher.min_weight_perfect_matching (matcher.py:78-88).
+ * rank 1: the Python solver is O(n^3) interpreted (63 s at n = 512).
+ *
+ * The solver is the O(n^3) primal-dual blossom algorithm on a dense complete
+ * graph, run in EXACT integer arithmetic: every weight is a finite double,
+ * scaled by a power of two into a 128-bit integer, so tightness tests are
+ * exact and the result is a true optimum of the given doubles.
+ */
+#ifndef COSCHED_MATCH_H
+#define COSCHED_MATCH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char *cm_version(void);
+
+/* Maximum-weight matching of the complete graph on n vertices with symmetric
+ * weights w[i*n + j] (diagonal ignored).  mate_out[v] = partner or -1.
+ * Returns 0, or -1 on bad input (non-finite / asymmetric / n < 0),
+ * -2 when weights span too many binary orders of magnitude for exact scaling. */
+int cm_max_weight_matching(const double *w, int32_t n, int32_t *mate_out);
+
+/* Minimum-weight perfect matching the reference's way (matcher.py:78-88):
+ * reflect r = (max(w) + 1) - w over the whole matrix (diagonal included, as
+ * numpy does), take the maximum-weight matching of r, which is perfect on a
+ * complete graph with an even vertex count.  mate_out as above.
+ * Returns 0, -1 on bad input (odd n, n < 2, non-finite, asymmetric), -2 as
+ * above, -3 if the matching came out imperfect (internal error). */
+int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,783 @@
+// sweep.cu -- sm_100a kernels + C ABI for the pair x knob sweep (include/cosched_b200.h).
+//
+// Pipeline per build_graph (scheduler.py:52-78), all stream-ordered:
+//   k_tables   factored layer-1 partials (fp64 + fp32 copies), one thread per row
+//   k_solo     per (budget, app) best exclusive split (estimator.py:139-180), fp64
+//   k_sweep    per (pair, config-slice) fp32 screen of every co-run config:
+//              z1 = (A_i + B_j) + K_c  ->  ReLU -> W2 (parameter bank) -> ReLU ->
+//              head -> floor 0.5 (estimator.py:98-109) -> x base_time -> max over
+//              members (estimator.py:127-129) -> per-budget (min, first index,
+//              runner-up) -> shuffle merge across slices -> fp64 re-evaluation of
+//              the winner -> co-run/solo decision (hwopt.py:77-87).  Raw
+//              predictions never leave registers.
+//   k_resolve  exact fp64 first-index argmin for the (rare) pairs whose fp32
+//              runner-up is within rel_eps of the minimum (hwopt.py:59 ties).
+//   k_scatter  symmetric N x N weights for PairGraph (scheduler.py:73-77).
+//
+// fp64 arithmetic uses explicit fma() in the same order as oracle/cosched_oracle.c,
+// so fp64 outputs are bit-identical to the C restatement of the reference.
+#include "cosched_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+namespace {
+
+constexpr int NF = CS_NUM_FEATURES;
+constexpr int HD = CS_HIDDEN;
+constexpr int IN = CS_INPUT_DIM;
+constexpr int ROW32 = 20;                  // fp32 table row: 18 + 2 pad (80 B, float4-aligned)
+constexpr int NET64_LEN = HD * HD + HD + HD + 1;  // w2 | b2 | w_out | b_out
+constexpr double FLOOR = 0.5;              // estimator.py:33
+constexpr int kSweepThreads = 128;
+
+// ---- kernel-parameter-bank network images ---------------------------------
+struct Net64P {          // 9.1 KB: needs the >4 KB kernel-parameter space (CUDA >= 12.1)
+    double w1[HD * IN];
+    double b1[HD];
+    double w2[HD * HD];
+    double b2[HD];
+    double wo[HD];
+    double bo;
+    double bounds[2 * NF];
+};
+
+struct Net32P {          // fp32 screen: W2 as FFMA constant-bank operands
+    float w2[HD * HD];
+    float b2[HD];
+    float wo[HD];
+    float bo;
+};
+
+struct GridP {
+    const double *knob1, *knob2, *solo_knob;
+    const uint32_t *mask;
+    int32_t G, L, S;
+    int32_t solo_off[CS_MAX_BUDGETS + 1];
+};
+
+GridP grid_params(const cs_grid *g) {
+    GridP p;
+    p.knob1 = g->knob1; p.knob2 = g->knob2; p.solo_knob = g->solo_knob; p.mask = g->mask;
+    p.G = g->n_grid; p.L = g->n_budgets; p.S = g->solo_offsets[g->n_budgets];
+    for (int l = 0; l <= CS_MAX_BUDGETS; ++l) p.solo_off[l] = l <= g->n_budgets ? g->solo_offsets[l] : p.S;
+    return p;
+}
+
+bool net64_from(const cs_network *net, Net64P *p) {
+    if (!net || !net->w1 || !net->b1 || !net->w2 || !net->b2 || !net->w_out || !net->b_out ||
+        !net->feature_bounds)
+        return false;
+    memcpy(p->w1, net->w1, sizeof(p->w1));
+    memcpy(p->b1, net->b1, sizeof(p->b1));
+    memcpy(p->w2, net->w2, sizeof(p->w2));
+    memcpy(p->b2, net->b2, sizeof(p->b2));
+    memcpy(p->wo, net->w_out, sizeof(p->wo));
+    p->bo = net->b_out[0];
+    memcpy(p->bounds, net->feature_bounds, sizeof(p->bounds));
+    return true;
+}
+
+// ---- pair index <-> (i, j), row-major i < j (scheduler.py:61) -------------
+__host__ __device__ __forceinline__ int64_t row_start(int64_t i, int64_t n) {
+    return i * (2 * n - i - 1) / 2;
+}
+
+__device__ __forceinline__ void pair_of(int64_t p, int n, int &i, int &j) {
+    double b = 2.0 * n - 1.0;
+    double disc = b * b - 8.0 * (double)p;
+    int ii = (int)floor((b - sqrt(fmax(disc, 0.0))) * 0.5);
+    ii = max(0, min(ii, n - 2));
+    while (ii > 0 && row_start(ii, n) > p) --ii;
+    while (ii < n - 2 && row_start(ii + 1, n) <= p) ++ii;
+    i = ii;
+    j = (int)(p - row_start(ii, n)) + ii + 1;
+}
+
+// ---- fp64 exact path (mirrors orc_head in oracle/cosched_oracle.c) --------
+// net64 layout: w2[324] | b2[18] | wo[18] | bo
+__device__ __forceinline__ double head64(const double *__restrict__ net, const double *z) {
+    double h1[HD];
+#pragma unroll
+    for (int k = 0; k < HD; ++k) h1[k] = z[k] > 0.0 ? z[k] : 0.0;
+    double y = 0.0;
+#pragma unroll 3
+    for (int o = 0; o < HD; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < HD; ++k) acc = fma(h1[k], __ldg(net + o * HD + k), acc);
+        acc = acc + __ldg(net + HD * HD + o);
+        y = fma(acc > 0.0 ? acc : 0.0, __ldg(net + HD * HD + HD + o), y);
+    }
+    y = y + __ldg(net + HD * HD + 2 * HD);
+    return y > 0.0 ? y : 0.0;
+}
+
+// CoRunTime of one config for pair (i, j): max over members of floor(pred) x T.
+__device__ double corun64(const cs_tables &t, const double *__restrict__ base_time, int i, int j,
+                          int c) {
+    double z[HD];
+    const double *ai = t.app_a64 + (size_t)i * HD, *bj = t.app_b64 + (size_t)j * HD;
+    const double *aj = t.app_a64 + (size_t)j * HD, *bi = t.app_b64 + (size_t)i * HD;
+    const double *k1 = t.knob1_64 + (size_t)c * HD, *k2 = t.knob2_64 + (size_t)c * HD;
+#pragma unroll
+    for (int h = 0; h < HD; ++h) z[h] = (__ldg(ai + h) + __ldg(bj + h)) + __ldg(k1 + h);
+    double y1 = head64(t.net64, z);
+#pragma unroll
+    for (int h = 0; h < HD; ++h) z[h] = (__ldg(aj + h) + __ldg(bi + h)) + __ldg(k2 + h);
+    double y2 = head64(t.net64, z);
+    double t1 = (y1 < FLOOR ? FLOOR : y1) * __ldg(base_time + i);
+    double t2 = (y2 < FLOOR ? FLOOR : y2) * __ldg(base_time + j);
+    return t1 > t2 ? t1 : t2;
+}
+
+// ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
+__device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+__global__ void k_tables(const __grid_constant__ Net64P net, const double *__restrict__ feats,
+                         int n, const GridP g, const cs_tables t) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid < NET64_LEN) {
+        double v;
+        if (tid < HD * HD) v = net.w2[tid];
+        else if (tid < HD * HD + HD) v = net.b2[tid - HD * HD];
+        else if (tid < HD * HD + 2 * HD) v = net.wo[tid - HD * HD - HD];
+        else v = net.bo;
+        t.net64[tid] = v;
+    }
+    const int64_t rows = (int64_t)n + g.G + g.S;
+    for (int64_t r = tid; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        if (r < n) {
+            double x1[NF], x2[NF];
+            const double *f = feats + r * NF;
+#pragma unroll
+            for (int k = 0; k < NF; ++k) {
+                x1[k] = clip01(f[k] / net.bounds[k]);
+                x2[k] = clip01(f[k] / net.bounds[NF + k]);
+            }
+            for (int h = 0; h < HD; ++h) {
+                double sa = 0.0, sb = 0.0;
+#pragma unroll
+                for (int k = 0; k < NF; ++k) {
+                    sa = fma(x1[k], net.w1[h * IN + 4 + k], sa);
+                    sb = fma(x2[k], net.w1[h * IN + 4 + NF + k], sb);
+                }
+                t.app_a64[r * HD + h] = sa;
+                t.app_b64[r * HD + h] = sb;
+                t.app_a32[r * ROW32 + h] = (float)sa;
+                t.app_b32[r * ROW32 + h] = (float)sb;
+            }
+            t.app_a32[r * ROW32 + 18] = t.app_a32[r * ROW32 + 19] = 0.f;
+            t.app_b32[r * ROW32 + 18] = t.app_b32[r * ROW32 + 19] = 0.f;
+        } else {
+            const bool solo = r >= (int64_t)n + g.G;
+            const int64_t c = solo ? r - n - g.G : r - n;
+            const int nviews = solo ? 1 : 2;
+            for (int v = 0; v < nviews; ++v) {
+                const double *kn = (solo ? g.solo_knob : (v == 0 ? g.knob1 : g.knob2)) + c * 4;
+                double kx[4] = {kn[0], kn[1], kn[2], kn[3]};
+                double *o64 = solo ? t.solo64 + c * HD
+                                   : (v == 0 ? t.knob1_64 : t.knob2_64) + c * HD;
+                float *o32 = solo ? nullptr : (v == 0 ? t.knob1_32 : t.knob2_32) + c * ROW32;
+                for (int h = 0; h < HD; ++h) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) s = fma(kx[k], net.w1[h * IN + k], s);
+                    s = s + net.b1[h];
+                    o64[h] = s;
+                    if (o32) o32[h] = (float)s;
+                }
+                if (o32) o32[18] = o32[19] = 0.f;
+            }
+        }
+    }
+}
+
+// ---- k_solo: per (budget, app) best split, fp64 (estimator.py:160-180) ----
+__global__ void k_solo(const cs_tables t, const GridP g, const double *__restrict__ base_time,
+                       int n, cs_solo_out out) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= (int64_t)n * g.L) return;
+    const int l = (int)(tid / n), a = (int)(tid % n);
+    double z[HD];
+    double best = 0.0;
+    int arg = -1, clamps = 0;
+    const double T = base_time[a];
+    for (int s = g.solo_off[l]; s < g.solo_off[l + 1]; ++s) {
+#pragma unroll
+        for (int h = 0; h < HD; ++h) z[h] = t.app_a64[(size_t)a * HD + h] + t.solo64[(size_t)s * HD + h];
+        double y = head64(t.net64, z);
+        if (y < FLOOR) { ++clamps; y = FLOOR; }
+        double tt = y * T;
+        if (arg < 0 || tt < best) { best = tt; arg = s - g.solo_off[l]; }
+    }
+    out.solo_time[tid] = arg < 0 ? nan("") : best;
+    out.solo_split[tid] = arg;
+    if (out.solo_clamps) out.solo_clamps[tid] = clamps;
+}
+
+// ---- k_sweep: fp32 screen of (pair, config) + fused reductions ------------
+struct SweepArgs {
+    cs_tables t;
+    GridP g;
+    const double *base_time, *solo_time;
+    const int32_t *solo_clamps;
+    int32_t n, log2s;
+    int64_t p_begin, P;
+    float eps;
+    cs_pair_out out;
+    int64_t *queue;
+    uint32_t *qcount;
+    unsigned long long *clamps;
+};
+
+__device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
+    float h[HD];
+#pragma unroll
+    for (int k = 0; k < HD; ++k) h[k] = fmaxf(z[k], 0.f);
+    float y = net.bo;
+#pragma unroll
+    for (int o = 0; o < HD; ++o) {
+        float acc = net.b2[o];
+#pragma unroll
+        for (int k = 0; k < HD; ++k) acc = fmaf(h[k], net.w2[o * HD + k], acc);
+        y = fmaf(fmaxf(acc, 0.f), net.wo[o], y);
+    }
+    return y;
+}
+
+__device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&r)[HD]) {
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    float4 v0 = __ldg(q), v1 = __ldg(q + 1), v2 = __ldg(q + 2), v3 = __ldg(q + 3), v4 = __ldg(q + 4);
+    r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
+    r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
+    r[8] = v2.x; r[9] = v2.y; r[10] = v2.z; r[11] = v2.w;
+    r[12] = v3.x; r[13] = v3.y; r[14] = v3.z; r[15] = v3.w;
+    r[16] = v4.x; r[17] = v4.y;
+}
+
+template <int L>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
+                                                         const __grid_constant__ Net32P net) {
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int S = 1 << a.log2s;
+    const int64_t pl = gt >> a.log2s;          // local pair index
+    const int s = (int)(gt & (S - 1));         // config slice
+    const bool live = pl < a.P;
+    int i = 0, j = 1;
+    if (live) pair_of(a.p_begin + pl, a.n, i, j);
+
+    float best[L], second[L];
+    int idx[L], clamps[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; clamps[l] = 0; }
+
+    if (live) {
+        float p1[HD], p2[HD], tmp[HD];
+        load_row20(a.t.app_a32 + (size_t)i * ROW32, p1);
+        load_row20(a.t.app_b32 + (size_t)j * ROW32, tmp);
+#pragma unroll
+        for (int h = 0; h < HD; ++h) p1[h] += tmp[h];
+        load_row20(a.t.app_a32 + (size_t)j * ROW32, p2);
+        load_row20(a.t.app_b32 + (size_t)i * ROW32, tmp);
+#pragma unroll
+        for (int h = 0; h < HD; ++h) p2[h] += tmp[h];
+        const float ti = (float)a.base_time[i], tj = (float)a.base_time[j];
+
+        for (int c = s; c < a.g.G; c += S) {
+            const uint32_t m = L == 1 ? 1u : __ldg(a.g.mask + c);
+            float z[HD];
+            load_row20(a.t.knob1_32 + (size_t)c * ROW32, z);
+#pragma unroll
+            for (int h = 0; h < HD; ++h) z[h] += p1[h];
+            const float y1 = head32(net, z);
+            load_row20(a.t.knob2_32 + (size_t)c * ROW32, z);
+#pragma unroll
+            for (int h = 0; h < HD; ++h) z[h] += p2[h];
+            const float y2 = head32(net, z);
+            const int cl = (y1 < 0.5f) + (y2 < 0.5f);
+            const float tt = fmaxf(fmaxf(y1, 0.5f) * ti, fmaxf(y2, 0.5f) * tj);
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                if (L == 1 || ((m >> l) & 1u)) {
+                    clamps[l] += cl;
+                    if (tt < best[l]) { second[l] = best[l]; best[l] = tt; idx[l] = c; }
+                    else second[l] = fminf(second[l], tt);
+                }
+            }
+        }
+    }
+
+    // merge the S slices of a pair (adjacent lanes): lexicographic (value, index)
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        for (int off = 1; off < S; off <<= 1) {
+            float ob = __shfl_xor_sync(0xffffffffu, best[l], off);
+            float os = __shfl_xor_sync(0xffffffffu, second[l], off);
+            int oi = __shfl_xor_sync(0xffffffffu, idx[l], off);
+            bool other = ob < best[l] || (ob == best[l] && oi < idx[l]);
+            float loser = other ? best[l] : ob;
+            second[l] = fminf(fminf(second[l], os), loser);
+            if (other) { best[l] = ob; idx[l] = oi; }
+        }
+        int tot = __reduce_add_sync(0xffffffffu, clamps[l]);
+        if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.clamps + l, (unsigned long long)tot);
+    }
+
+    if (!live || s != 0) return;
+#pragma unroll 1
+    for (int l = 0; l < L; ++l) {
+        if (a.solo_clamps)
+            atomicAdd(a.clamps + l, (unsigned long long)(a.solo_clamps[(size_t)l * a.n + i] +
+                                                         a.solo_clamps[(size_t)l * a.n + j]));
+        const int64_t o = (int64_t)l * a.P + pl;
+        const bool ambiguous = !(second[l] > best[l] * (1.0f + a.eps));
+        if (ambiguous) {
+            uint32_t q = atomicAdd(a.qcount, 1u);
+            a.queue[q] = (pl << 4) | l;
+            continue;
+        }
+        const int c = idx[l];
+        const double co = corun64(a.t, a.base_time, i, j, c);
+        const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
+        const bool chosen = co <= solo;                       // hwopt.py:86
+        a.out.corun_grid_index[o] = c;
+        a.out.corun_time[o] = co;
+        a.out.corun_chosen[o] = chosen;
+        a.out.weight[o] = chosen ? co : solo;
+        float gap = (float)(fabs(co - (double)best[l]) / co);
+        atomicMax(a.qcount + 1, __float_as_uint(gap));
+    }
+}
+
+// ---- k_resolve: exact fp64 argmin for queued (pair, budget) ---------------
+struct ResolveArgs {
+    cs_tables t;
+    GridP g;
+    const double *base_time, *solo_time;
+    int32_t n;
+    int64_t p_begin, P;
+    cs_pair_out out;
+    const int64_t *queue;
+    const uint32_t *qcount;
+};
+
+__global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a) {
+    const uint32_t count = *a.qcount;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = warp; q < count; q += nwarps) {
+        const int64_t e = a.queue[q];
+        const int64_t pl = e >> 4;
+        const int l = (int)(e & 15);
+        int i, j;
+        pair_of(a.p_begin + pl, a.n, i, j);
+        double best = INFINITY;
+        int arg = INT_MAX;
+        for (int c = lane; c < a.g.G; c += 32) {
+            if (!((__ldg(a.g.mask + c) >> l) & 1u)) continue;
+            double tt = corun64(a.t, a.base_time, i, j, c);
+            if (tt < best) { best = tt; arg = c; }          // ascending c per lane: first index
+        }
+        for (int off = 16; off; off >>= 1) {
+            double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            int oi = __shfl_xor_sync(0xffffffffu, arg, off);
+            if (ob < best || (ob == best && oi < arg)) { best = ob; arg = oi; }
+        }
+        if (lane == 0) {
+            const int64_t o = (int64_t)l * a.P + pl;
+            const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
+            const bool chosen = arg != INT_MAX && best <= solo;
+            a.out.corun_grid_index[o] = arg == INT_MAX ? -1 : arg;
+            a.out.corun_time[o] = best;
+            a.out.corun_chosen[o] = chosen;
+            a.out.weight[o] = chosen ? best : solo;
+        }
+    }
+}
+
+// ---- k_scatter: symmetric weight matrix ----------------------------------
+__global__ void k_scatter(const double *__restrict__ weight, int n, int64_t p_begin, int64_t P,
+                          double *__restrict__ W) {
+    for (int64_t pl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pl < P;
+         pl += (int64_t)gridDim.x * blockDim.x) {
+        int i, j;
+        pair_of(p_begin + pl, n, i, j);
+        const double w = weight[pl];
+        W[(size_t)i * n + j] = w;
+        W[(size_t)j * n + i] = w;
+    }
+}
+
+// ---- k_forward_rows: fnn.forward_batch, fp64 (fnn.py:161-165) -------------
+__global__ void k_forward_rows(const __grid_constant__ Net64P net, const double *__restrict__ x,
+                               int64_t rows, double *__restrict__ y) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const double *xr = x + r * IN;
+        double h1[HD];
+        for (int h = 0; h < HD; ++h) {
+            double acc = 0.0;
+            for (int k = 0; k < IN; ++k) acc = fma(xr[k], net.w1[h * IN + k], acc);
+            acc = acc + net.b1[h];
+            h1[h] = acc > 0.0 ? acc : 0.0;
+        }
+        double out = 0.0;
+        for (int o = 0; o < HD; ++o) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < HD; ++k) acc = fma(h1[k], net.w2[o * HD + k], acc);
+            acc = acc + net.b2[o];
+            out = fma(acc > 0.0 ? acc : 0.0, net.wo[o], out);
+        }
+        out = out + net.bo;
+        y[r] = out > 0.0 ? out : 0.0;
+    }
+}
+
+int sm_count() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
+int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "cosched_b200: CUDA error: %s\n", cudaGetErrorString(e));
+        return CS_ERR_CUDA;
+    }
+    return CS_OK;
+}
+
+int check_grid(const cs_grid *g) {
+    if (!g || g->n_grid < 0 || g->n_budgets < 1 || g->n_budgets > CS_MAX_BUDGETS) return CS_ERR_ARG;
+    if (g->n_grid > 0 && (!g->knob1 || !g->knob2 || !g->mask)) return CS_ERR_ARG;
+    // Empty budgets are legal here (the reference's optimize_corun works on a
+    // budget without solo splits and optimize_solo_pair on one without co-run
+    // configs); their records come out as index -1 / NaN and the host raises
+    // CS_ERR_NO_CONFIG / CS_ERR_UNREACHABLE semantics only for what it reads.
+    for (int l = 0; l < g->n_budgets; ++l) {
+        if (g->solo_offsets[l + 1] < g->solo_offsets[l] || g->n_configs[l] < 0) return CS_ERR_ARG;
+    }
+    if (g->solo_offsets[0] != 0 || (g->solo_offsets[g->n_budgets] > 0 && !g->solo_knob)) return CS_ERR_ARG;
+    return CS_OK;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+int choose_log2_slices(int64_t P, int G) {
+    // enough (pair, slice) threads to fill the SMs about twice over, but
+    // keep >= ~4 configs per slice so the per-thread prologue stays amortized
+    const int64_t target = (int64_t)sm_count() * 2048;
+    int l2 = 0;
+    while (l2 < 3 && P * (1LL << l2) < target && (G >> (l2 + 1)) >= 4) ++l2;
+    return l2;
+}
+
+template <int L>
+void launch_sweep(const SweepArgs &a, const Net32P &net, cudaStream_t st) {
+    const int64_t threads = a.P << a.log2s;
+    const int64_t blocks = (threads + kSweepThreads - 1) / kSweepThreads;
+    k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net);
+}
+
+}  // namespace
+
+// =========================================================================
+// C ABI
+// =========================================================================
+extern "C" {
+
+const char *cs_version(void) { return "cosched_b200 0.1.0 (sm_100a)"; }
+
+const char *cs_error_string(int code) {
+    switch (code) {
+        case CS_OK: return "ok";
+        case CS_ERR_ARG: return "invalid argument";
+        case CS_ERR_NO_CONFIG: return "no co-run configs exist for a requested budget";
+        case CS_ERR_UNREACHABLE: return "budget is unreachable on the cap grids (no solo split)";
+        case CS_ERR_CUDA: return "CUDA runtime error";
+        case CS_ERR_WORKSPACE: return "workspace too small";
+        default: return "unknown error";
+    }
+}
+
+size_t cs_tables_bytes(int32_t n_apps, int32_t n_grid, int32_t n_solo) {
+    if (n_apps < 0 || n_grid < 0 || n_solo < 0) return 0;
+    size_t b = 0;
+    b += align256(sizeof(double) * NET64_LEN);
+    b += 2 * align256(sizeof(float) * (size_t)n_apps * ROW32);
+    b += 2 * align256(sizeof(double) * (size_t)n_apps * HD);
+    b += 2 * align256(sizeof(float) * (size_t)n_grid * ROW32);
+    b += 2 * align256(sizeof(double) * (size_t)n_grid * HD);
+    b += align256(sizeof(double) * (size_t)n_solo * HD);
+    return b;
+}
+
+int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, int32_t n_solo,
+                   cs_tables *out) {
+    if (!d_base || !out || ((uintptr_t)d_base & 255)) return CS_ERR_ARG;
+    if (bytes < cs_tables_bytes(n_apps, n_grid, n_solo)) return CS_ERR_WORKSPACE;
+    char *p = (char *)d_base;
+    auto take = [&p](size_t sz) { char *r = p; p += align256(sz); return (void *)r; };
+    out->n_apps = n_apps; out->n_grid = n_grid; out->n_solo = n_solo;
+    out->net64 = (double *)take(sizeof(double) * NET64_LEN);
+    out->app_a32 = (float *)take(sizeof(float) * (size_t)n_apps * ROW32);
+    out->app_b32 = (float *)take(sizeof(float) * (size_t)n_apps * ROW32);
+    out->app_a64 = (double *)take(sizeof(double) * (size_t)n_apps * HD);
+    out->app_b64 = (double *)take(sizeof(double) * (size_t)n_apps * HD);
+    out->knob1_32 = (float *)take(sizeof(float) * (size_t)n_grid * ROW32);
+    out->knob2_32 = (float *)take(sizeof(float) * (size_t)n_grid * ROW32);
+    out->knob1_64 = (double *)take(sizeof(double) * (size_t)n_grid * HD);
+    out->knob2_64 = (double *)take(sizeof(double) * (size_t)n_grid * HD);
+    out->solo64 = (double *)take(sizeof(double) * (size_t)n_solo * HD);
+    return CS_OK;
+}
+
+int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
+                    const cs_grid *d_grid, const cs_tables *tables, void *stream) {
+    Net64P np;
+    if (!net64_from(net, &np) || !tables || n_apps < 2 || !d_features) return CS_ERR_ARG;
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    GridP g = grid_params(d_grid);
+    if (tables->n_apps != n_apps || tables->n_grid != g.G || tables->n_solo < g.S) return CS_ERR_ARG;
+    const int64_t rows = (int64_t)n_apps + g.G + g.S;
+    int64_t threads = rows > NET64_LEN ? rows : NET64_LEN;
+    int blocks = (int)((threads + 127) / 128);
+    k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables);
+    return check_launch();
+}
+
+int cs_solo(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
+            cs_solo_out out, void *stream) {
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    if (!tables || !d_base_time || !out.solo_time || !out.solo_split) return CS_ERR_ARG;
+    GridP g = grid_params(d_grid);
+    const int64_t threads = (int64_t)tables->n_apps * g.L;
+    k_solo<<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        *tables, g, d_base_time, tables->n_apps, out);
+    return check_launch();
+}
+
+int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                  const double *d_base_time, const double *d_solo_time,
+                  const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                  double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                  unsigned long long *d_clamps, void *stream) {
+    Net64P n64;
+    if (!net64_from(net, &n64)) return CS_ERR_ARG;
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count || !d_clamps ||
+        !out.corun_grid_index || !out.corun_time || !out.corun_chosen || !out.weight)
+        return CS_ERR_ARG;
+    const int64_t n = tables->n_apps;
+    const int64_t P_all = n * (n - 1) / 2;
+    if (pair_begin < 0 || pair_end > P_all || pair_begin > pair_end) return CS_ERR_ARG;
+    if (!(rel_eps > 0.0 && rel_eps < 0.1)) return CS_ERR_ARG;
+    if (pair_begin == pair_end) return CS_OK;
+
+    Net32P n32;
+    for (int k = 0; k < HD * HD; ++k) n32.w2[k] = (float)n64.w2[k];
+    for (int k = 0; k < HD; ++k) { n32.b2[k] = (float)n64.b2[k]; n32.wo[k] = (float)n64.wo[k]; }
+    n32.bo = (float)n64.bo;
+
+    SweepArgs a;
+    a.t = *tables;
+    a.g = grid_params(d_grid);
+    a.base_time = d_base_time;
+    a.solo_time = d_solo_time;
+    a.solo_clamps = d_solo_clamps;
+    a.n = (int32_t)n;
+    a.p_begin = pair_begin;
+    a.P = pair_end - pair_begin;
+    a.log2s = choose_log2_slices(a.P, a.g.G);
+    a.eps = (float)rel_eps;
+    a.out = out;
+    a.queue = d_queue;
+    a.qcount = d_queue_count;
+    a.clamps = d_clamps;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (a.g.L) {
+        case 1: launch_sweep<1>(a, n32, st); break;
+        case 2: launch_sweep<2>(a, n32, st); break;
+        case 3: launch_sweep<3>(a, n32, st); break;
+        case 4: launch_sweep<4>(a, n32, st); break;
+        case 5: launch_sweep<5>(a, n32, st); break;
+        case 6: launch_sweep<6>(a, n32, st); break;
+        case 7: launch_sweep<7>(a, n32, st); break;
+        case 8: launch_sweep<8>(a, n32, st); break;
+        default: return CS_ERR_ARG;
+    }
+    return check_launch();
+}
+
+int cs_resolve(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
+               const double *d_solo_time, int64_t pair_begin, int64_t pair_end,
+               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+               void *stream) {
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count) return CS_ERR_ARG;
+    if (pair_begin == pair_end) return CS_OK;
+    ResolveArgs a;
+    a.t = *tables;
+    a.g = grid_params(d_grid);
+    a.base_time = d_base_time;
+    a.solo_time = d_solo_time;
+    a.n = tables->n_apps;
+    a.p_begin = pair_begin;
+    a.P = pair_end - pair_begin;
+    a.out = out;
+    a.queue = d_queue;
+    a.qcount = d_queue_count;
+    // the queue length lives on the device: launch one resident wave, grid-stride
+    k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a);
+    return check_launch();
+}
+
+int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,
+                       int64_t pair_end, double *d_w, void *stream) {
+    if (!d_weight || !d_w || n_apps < 2 || pair_begin < 0 || pair_end < pair_begin ||
+        pair_end > (int64_t)n_apps * (n_apps - 1) / 2)
+        return CS_ERR_ARG;
+    const int64_t P = pair_end - pair_begin;
+    if (!P) return CS_OK;
+    int64_t blocks = (P + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+    k_scatter<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_weight, n_apps, pair_begin, P, d_w);
+    return check_launch();
+}
+
+int cs_forward_rows(const cs_network *net, const double *d_x, int64_t rows, double *d_y,
+                    void *stream) {
+    Net64P np;
+    if (!net64_from(net, &np) || rows < 0 || (rows > 0 && (!d_x || !d_y))) return CS_ERR_ARG;
+    if (!rows) return CS_OK;
+    int64_t blocks = (rows + 127) / 128;
+    if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
+    k_forward_rows<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(np, d_x, rows, d_y);
+    return check_launch();
+}
+
+// ---- host-buffer build_graph ---------------------------------------------
+namespace {
+struct GraphLayout {
+    size_t feats, bt, knob1, knob2, mask, solo_knob, tables, solo_time, solo_split, solo_clamps,
+        corun_idx, corun_time, chosen, weight, queue, qcount, clamps, W, total;
+};
+
+GraphLayout graph_layout(int32_t n, const cs_grid *g) {
+    GraphLayout L{};
+    const int64_t P = (int64_t)n * (n - 1) / 2;
+    const int64_t nb = g->n_budgets, G = g->n_grid, S = g->solo_offsets[g->n_budgets];
+    size_t off = 0;
+    auto put = [&off](size_t sz) { size_t r = off; off += align256(sz); return r; };
+    L.feats = put(sizeof(double) * (size_t)n * NF);
+    L.bt = put(sizeof(double) * (size_t)n);
+    L.knob1 = put(sizeof(double) * (size_t)G * 4);
+    L.knob2 = put(sizeof(double) * (size_t)G * 4);
+    L.mask = put(sizeof(uint32_t) * (size_t)G);
+    L.solo_knob = put(sizeof(double) * (size_t)S * 4);
+    L.tables = put(cs_tables_bytes(n, (int32_t)G, (int32_t)S));
+    L.solo_time = put(sizeof(double) * (size_t)(nb * n));
+    L.solo_split = put(sizeof(int32_t) * (size_t)(nb * n));
+    L.solo_clamps = put(sizeof(int32_t) * (size_t)(nb * n));
+    L.corun_idx = put(sizeof(int32_t) * (size_t)(nb * P));
+    L.corun_time = put(sizeof(double) * (size_t)(nb * P));
+    L.chosen = put(sizeof(uint8_t) * (size_t)(nb * P));
+    L.weight = put(sizeof(double) * (size_t)(nb * P));
+    L.queue = put(sizeof(int64_t) * (size_t)(nb * P));
+    L.qcount = put(sizeof(uint32_t) * 2);
+    L.clamps = put(sizeof(unsigned long long) * (size_t)nb);
+    L.W = put(sizeof(double) * (size_t)n * n);
+    L.total = off;
+    return L;
+}
+}  // namespace
+
+size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid) {
+    if (n_apps < 2 || check_grid(h_grid) != CS_OK) return 0;
+    return graph_layout(n_apps, h_grid).total;
+}
+
+int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
+                        const double *h_base_time, int32_t n_apps, double rel_eps,
+                        void *d_workspace, size_t workspace_bytes, double *h_weights,
+                        cs_pair_out h_pairs, cs_solo_out h_solo,
+                        unsigned long long *h_clamps, void *stream) {
+    if (!net || !h_features || !h_base_time || n_apps < 2 || !d_workspace) return CS_ERR_ARG;
+    int rc = check_grid(h_grid);
+    if (rc) return rc;
+    const GraphLayout L = graph_layout(n_apps, h_grid);
+    if (workspace_bytes < L.total) return CS_ERR_WORKSPACE;
+    if ((uintptr_t)d_workspace & 255) return CS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    char *ws = (char *)d_workspace;
+    const int64_t P = (int64_t)n_apps * (n_apps - 1) / 2;
+    const int nb = h_grid->n_budgets, G = h_grid->n_grid, S = h_grid->solo_offsets[nb];
+    const size_t n = (size_t)n_apps;
+#define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { \
+        fprintf(stderr, "cosched_b200: %s\n", cudaGetErrorString(_e)); return CS_ERR_CUDA; } } while (0)
+#define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
+    CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
+    CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    if (G) {
+        CS_TRY(cudaMemcpyAsync(ws + L.knob1, h_grid->knob1, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
+        CS_TRY(cudaMemcpyAsync(ws + L.knob2, h_grid->knob2, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
+        CS_TRY(cudaMemcpyAsync(ws + L.mask, h_grid->mask, sizeof(uint32_t) * G, cudaMemcpyHostToDevice, st));
+    }
+    if (S) CS_TRY(cudaMemcpyAsync(ws + L.solo_knob, h_grid->solo_knob, sizeof(double) * S * 4, cudaMemcpyHostToDevice, st));
+    CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, sizeof(uint32_t) * 2, st));
+    CS_TRY(cudaMemsetAsync(ws + L.clamps, 0, sizeof(unsigned long long) * nb, st));
+
+    cs_grid dg = *h_grid;
+    dg.knob1 = (const double *)(ws + L.knob1);
+    dg.knob2 = (const double *)(ws + L.knob2);
+    dg.mask = (const uint32_t *)(ws + L.mask);
+    dg.solo_knob = (const double *)(ws + L.solo_knob);
+    cs_tables t;
+    CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
+    CS_RC(cs_build_tables(net, (const double *)(ws + L.feats), n_apps, &dg, &t, stream));
+    cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
+                   (int32_t *)(ws + L.solo_clamps)};
+    CS_RC(cs_solo(&t, &dg, (const double *)(ws + L.bt), so, stream));
+    cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
+                   (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
+    CS_RC(cs_pair_sweep(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time, so.solo_clamps, 0, P,
+                        rel_eps, po, (int64_t *)(ws + L.queue), (uint32_t *)(ws + L.qcount),
+                        (unsigned long long *)(ws + L.clamps), stream));
+    CS_RC(cs_resolve(&t, &dg, (const double *)(ws + L.bt), so.solo_time, 0, P, po,
+                     (const int64_t *)(ws + L.queue), (const uint32_t *)(ws + L.qcount), stream));
+    for (int l = 0; l < nb && h_weights; ++l) {
+        CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n, st));
+        CS_RC(cs_scatter_weights(po.weight + (size_t)l * P, n_apps, 0, P, (double *)(ws + L.W), stream));
+        CS_TRY(cudaMemcpyAsync(h_weights + (size_t)l * n * n, ws + L.W, sizeof(double) * n * n,
+                               cudaMemcpyDeviceToHost, st));
+    }
+    const size_t LP = (size_t)nb * P, LN = (size_t)nb * n;
+    if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP, cudaMemcpyDeviceToHost, st));
+    if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));
+    if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen, po.corun_chosen, LP, cudaMemcpyDeviceToHost, st));
+    if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight, po.weight, 8 * LP, cudaMemcpyDeviceToHost, st));
+    if (h_solo.solo_time) CS_TRY(cudaMemcpyAsync(h_solo.solo_time, so.solo_time, 8 * LN, cudaMemcpyDeviceToHost, st));
+    if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
+    if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
+    if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
+    CS_TRY(cudaStreamSynchronize(st));
+#undef CS_TRY
+#undef CS_RC
+    return CS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+"""Device-side driver of the sweep: buffers, launches, results.
+
+PyTorch is plumbing here -- device memory, the current CUDA stream and (for
+multi-GPU) ``torch.distributed``.  Every kernel is ours, launched through the
+C ABI of ``libcosched_b200.so``; there is no CPU path for the FNN sweep and a
+missing extension or device raises.
+
+``SweepPlan`` owns every buffer of one (apps, grid, pair-shard) shape so that
+repeated sweeps (the bench loop, a scheduler serving many windows of the same
+size) launch kernels only:
+
+    k_tables -> k_solo -> k_sweep -> k_resolve [-> k_scatter per budget]
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import NUM_FEATURES, ValidationError
+from .grid import KnobGrid
+
+# Relative gap below which the fp32 screen defers to the exact fp64 re-scan.
+# The measured fp32 screen error is ~3e-7 relative (SURVEY.md §7 hard part 1);
+# the kernel reports the largest gap it saw (SweepPlan.screen_error) and
+# SweepPlan.launch() callers can assert it stays far below this.
+DEFAULT_REL_EPS = 1e-4
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the cosched_b200 sweep needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise RuntimeError(f"cosched_b200 runs on CUDA devices only, got {dev}")
+    return dev
+
+
+def _dptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class NetworkABI:
+    """Keeps the fp64 host arrays behind a cs_network alive."""
+
+    def __init__(self, weights):
+        self.arrays = weights.abi_arrays()
+        a = self.arrays
+        self.struct = nat.CsNetwork(*(nat.ptr(a[k]) for k in
+                                      ("w1", "b1", "w2", "b2", "w_out", "b_out", "feature_bounds")))
+
+    def ref(self):
+        return ctypes.byref(self.struct)
+
+
+class DeviceGrid:
+    """A KnobGrid's arrays resident on one device, plus its cs_grid struct."""
+
+    def __init__(self, grid: KnobGrid, device):
+        self.grid = grid
+        self.knob1 = torch.as_tensor(grid.knob1, device=device).contiguous()
+        self.knob2 = torch.as_tensor(grid.knob2, device=device).contiguous()
+        self.mask = torch.as_tensor(grid.mask.view(np.int32), device=device).contiguous()
+        solo = grid.solo_knob if len(grid.solo_knob) else np.zeros((1, 4))
+        self.solo_knob = torch.as_tensor(solo, device=device).contiguous()
+        s = nat.CsGrid()
+        s.n_grid = grid.n_grid
+        s.knob1 = ctypes.cast(_dptr(self.knob1), nat.c_double_p)
+        s.knob2 = ctypes.cast(_dptr(self.knob2), nat.c_double_p)
+        s.mask = ctypes.cast(_dptr(self.mask), nat.c_uint32_p)
+        s.n_budgets = grid.n_budgets
+        for l in range(grid.n_budgets):
+            s.n_configs[l] = grid.n_configs[l]
+        for l, off in enumerate(grid.solo_offsets):
+            s.solo_offsets[l] = off
+        s.solo_knob = ctypes.cast(_dptr(self.solo_knob), nat.c_double_p)
+        self.struct = s
+
+    def ref(self):
+        return ctypes.byref(self.struct)
+
+
+def n_pairs(n: int) -> int:
+    return n * (n - 1) // 2
+
+
+@dataclass
+class SweepCounters:
+    queue_len: int
+    screen_error: float
+    clamps: np.ndarray
+
+
+class SweepPlan:
+    """All device buffers for sweeping `n` apps over `grid`, pairs [begin, end)."""
+
+    def __init__(self, weights, grid: KnobGrid, n: int, pair_begin: int = 0,
+                 pair_end: Optional[int] = None, device=None, with_matrix: bool = True,
+                 rel_eps: float = DEFAULT_REL_EPS):
+        self.lib = nat.sweep_lib()
+        self.device = require_cuda(device)
+        if n < 2:
+            raise ValidationError(f"need at least 2 apps, got {n}")
+        P_all = n_pairs(n)
+        pair_end = P_all if pair_end is None else int(pair_end)
+        if not 0 <= pair_begin <= pair_end <= P_all:
+            raise ValidationError(f"pair range [{pair_begin}, {pair_end}) outside [0, {P_all})")
+        self.n, self.grid, self.rel_eps = n, grid, float(rel_eps)
+        self.pair_begin, self.pair_end = int(pair_begin), pair_end
+        self.P = pair_end - pair_begin
+        self.net = NetworkABI(weights)
+        dev = self.device
+        with torch.cuda.device(dev):
+            self.dgrid = DeviceGrid(grid, dev)
+            L, G, S = grid.n_budgets, grid.n_grid, grid.solo_offsets[-1]
+            nbytes = self.lib.cs_tables_bytes(n, G, S)
+            self.table_buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+            base = (_dptr(self.table_buf) + 255) & ~255
+            self.tables = nat.CsTables()
+            nat.check(self.lib.cs_tables_bind(base, nbytes, n, G, S, ctypes.byref(self.tables)),
+                      "cs_tables_bind")
+            P = max(self.P, 1)
+            self.corun_grid_index = torch.empty((L, P), dtype=torch.int32, device=dev)
+            self.corun_time = torch.empty((L, P), dtype=torch.float64, device=dev)
+            self.corun_chosen = torch.empty((L, P), dtype=torch.uint8, device=dev)
+            self.weight = torch.empty((L, P), dtype=torch.float64, device=dev)
+            self.solo_time = torch.empty((L, n), dtype=torch.float64, device=dev)
+            self.solo_split = torch.empty((L, n), dtype=torch.int32, device=dev)
+            self.solo_clamps = torch.empty((L, n), dtype=torch.int32, device=dev)
+            self.queue = torch.empty(L * P, dtype=torch.int64, device=dev)
+            self.counters = torch.zeros(2, dtype=torch.int32, device=dev)
+            self.clamps = torch.zeros(L, dtype=torch.int64, device=dev)
+            self.matrix = (torch.zeros((L, n, n), dtype=torch.float64, device=dev)
+                           if with_matrix else None)
+        self.pair_out = nat.CsPairOut(
+            ctypes.cast(_dptr(self.corun_grid_index), nat.c_int32_p),
+            ctypes.cast(_dptr(self.corun_time), nat.c_double_p),
+            ctypes.cast(_dptr(self.corun_chosen), nat.c_uint8_p),
+            ctypes.cast(_dptr(self.weight), nat.c_double_p))
+        self.solo_out = nat.CsSoloOut(
+            ctypes.cast(_dptr(self.solo_time), nat.c_double_p),
+            ctypes.cast(_dptr(self.solo_split), nat.c_int32_p),
+            ctypes.cast(_dptr(self.solo_clamps), nat.c_int32_p))
+        self.launches_per_run = 4 + (grid.n_budgets if with_matrix else 0)
+
+    # ------------------------------------------------------------------
+    def launch(self, d_features: torch.Tensor, d_base_time: torch.Tensor,
+               sweep_events: Optional[tuple] = None) -> None:
+        """Enqueue one full sweep on the current stream (no host sync).
+
+        `sweep_events` = (start, end) CUDA events recorded around the k_sweep
+        launch only (bench.py times the dominant kernel with them; create them
+        with external=True when the launch is captured into a CUDA graph)."""
+        n = self.n
+        if d_features.shape != (n, NUM_FEATURES) or d_base_time.shape != (n,):
+            raise ValidationError(f"expected features ({n}, 18) and base_time ({n},)")
+        if d_features.dtype != torch.float64 or d_base_time.dtype != torch.float64:
+            raise ValidationError("features and base_time must be float64")
+        if not (d_features.is_contiguous() and d_base_time.is_contiguous()):
+            raise ValidationError("features and base_time must be contiguous")
+        lib, dev = self.lib, self.device
+        st = _stream_handle(dev)
+        self.counters.zero_()
+        self.clamps.zero_()
+        tref = ctypes.byref(self.tables)
+        nat.check(lib.cs_build_tables(self.net.ref(), _dptr(d_features), n, self.dgrid.ref(),
+                                      tref, st), "cs_build_tables")
+        nat.check(lib.cs_solo(tref, self.dgrid.ref(), _dptr(d_base_time), self.solo_out, st),
+                  "cs_solo")
+        if self.P == 0:
+            return
+        cnt = _dptr(self.counters)
+        if sweep_events is not None:
+            sweep_events[0].record()
+        nat.check(lib.cs_pair_sweep(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
+                                    _dptr(self.solo_time), _dptr(self.solo_clamps),
+                                    self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
+                                    _dptr(self.queue), cnt, _dptr(self.clamps), st),
+                  "cs_pair_sweep")
+        if sweep_events is not None:
+            sweep_events[1].record()
+        nat.check(lib.cs_resolve(tref, self.dgrid.ref(), _dptr(d_base_time), _dptr(self.solo_time),
+                                 self.pair_begin, self.pair_end, self.pair_out, _dptr(self.queue),
+                                 cnt, st), "cs_resolve")
+        if self.matrix is not None:
+            self.scatter(st)
+
+    def scatter(self, st=None) -> None:
+        st = _stream_handle(self.device) if st is None else st
+        P = self.P
+        for l in range(self.grid.n_budgets):
+            nat.check(self.lib.cs_scatter_weights(
+                _dptr(self.weight) + 8 * l * max(P, 1), self.n, self.pair_begin, self.pair_end,
+                _dptr(self.matrix) + 8 * l * self.n * self.n, st), "cs_scatter_weights")
+
+    def read_counters(self) -> SweepCounters:
+        c = self.counters.cpu().numpy()
+        return SweepCounters(queue_len=int(c[0]),
+                             screen_error=float(np.array([c[1]], dtype=np.int32).view(np.float32)[0]),
+                             clamps=self.clamps.cpu().numpy().astype(np.int64))
+
+
+def to_device_inputs(features, base_time, device) -> tuple:
+    f = torch.as_tensor(np.ascontiguousarray(features, dtype=np.float64)).to(device, non_blocking=True)
+    b = torch.as_tensor(np.ascontiguousarray(base_time, dtype=np.float64)).to(device, non_blocking=True)
+    return f.contiguous(), b.contiguous()
+
+
+def forward_rows(weights, X: np.ndarray) -> np.ndarray:
+    """fnn.forward_batch on the GPU (fp64, unfloored)."""
+    lib = nat.sweep_lib()
+    dev = require_cuda()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    rows = X.shape[0]
+    if rows == 0:
+        return np.zeros(0)
+    net = NetworkABI(weights)
+    dx = torch.as_tensor(X).to(dev)
+    dy = torch.empty(rows, dtype=torch.float64, device=dev)
+    nat.check(lib.cs_forward_rows(net.ref(), _dptr(dx), rows, _dptr(dy), _stream_handle(dev)),
+              "cs_forward_rows")
+    return dy.cpu().numpy()

@@ -1,0 +1,189 @@
+"""End-to-end scheduling of a job queue (mirrors ``cosched.scheduler``).
+
+``build_graph`` (scheduler.py:52-78) is the hot path's driver.  For a trained
+network it is ONE fused GPU sweep over all N(N-1)/2 pairs (``sweep_pairs``):
+the symmetric weight matrix is scattered on the device and the per-edge
+``PairDecision``s are built lazily from the result arrays on access
+(``PairDecisions``), so the 8.4M-pair case never materializes Python objects
+it does not need.  ``schedule`` (81-107) matches on the host (native blossom)
+and emits job sets exactly as the reference does.
+"""
+
+from __future__ import annotations
+
+import json
+from collections.abc import Mapping
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import estimator
+from .core import ConfigSpace, HardwareConfig, JobSet, Schedule, SchedulingParams, ValidationError, solo_config
+from .hwopt import PairDecision, decide_pair
+from .matcher import PairGraph, min_weight_perfect_matching
+
+
+@dataclass(frozen=True)
+class SchedulerInput:
+    """Queued jobs, knob space, window parameters and the model (scheduler.py:32-49)."""
+
+    queue: tuple
+    space: ConfigSpace
+    params: SchedulingParams
+    model: object
+
+    def __post_init__(self) -> None:
+        queue = tuple(self.queue)
+        if not queue:
+            raise ValidationError("queue must not be empty")
+        if len(queue) != self.params.window:
+            raise ValidationError(
+                f"queue length {len(queue)} must equal the window {self.params.window}")
+        object.__setattr__(self, "queue", queue)
+
+
+def pair_index(n: int, i: int, j: int) -> int:
+    """Row-major linear index of the unordered pair i < j (scheduler.py:61)."""
+    return i * (2 * n - i - 1) // 2 + (j - i - 1)
+
+
+class PairDecisions(Mapping):
+    """Lazy ``{(i, j): PairDecision}`` view over one budget of a SweepResult."""
+
+    def __init__(self, result, budget: int = 0):
+        self._r = result
+        self._l = budget
+        self._n = result.n
+        self._splits = result.grid.solo_splits[budget]
+        self._cfg_cache: dict = {}
+
+    def __len__(self) -> int:
+        return self._n * (self._n - 1) // 2
+
+    def __iter__(self):
+        n = self._n
+        for i in range(n):
+            for j in range(i + 1, n):
+                yield (i, j)
+
+    def __contains__(self, key) -> bool:
+        try:
+            i, j = key
+        except (TypeError, ValueError):
+            return False
+        return isinstance(i, (int, np.integer)) and isinstance(j, (int, np.integer)) \
+            and 0 <= i < j < self._n
+
+    def _config(self, g: int) -> HardwareConfig:
+        hc = self._cfg_cache.get(g)
+        if hc is None:
+            hc = HardwareConfig(*self._r.grid.configs[g])
+            self._cfg_cache[g] = hc
+        return hc
+
+    def __getitem__(self, key) -> PairDecision:
+        if key not in self:
+            raise KeyError(key)
+        i, j = int(key[0]), int(key[1])
+        r, l = self._r, self._l
+        p = pair_index(self._n, i, j) - r.pair_begin
+        g = int(r.corun_grid_index[l, p])
+        st = r.solo_time[l]
+        si, sj = int(r.solo_split[l, i]), int(r.solo_split[l, j])
+        return PairDecision(
+            corun_config=self._config(g),
+            corun_time_s=float(r.corun_time[l, p]),
+            solo_configs=(solo_config(*self._splits[si]), solo_config(*self._splits[sj])),
+            solo_time_s=float((0.0 + st[i]) + st[j]),
+            corun_chosen=bool(r.corun_chosen[l, p]))
+
+
+def build_graph_gpu(jobs: Sequence, space: ConfigSpace, weights) -> PairGraph:
+    """The fused GPU sweep as a PairGraph (lazy decisions); updates clamp_stats."""
+    from .sweep import sweep_pairs
+    res = sweep_pairs(weights, jobs, space, with_matrix=True)
+    estimator.clamp_stats.count += int(res.clamps[0])
+    return PairGraph.trusted(res.matrix[0], PairDecisions(res, 0))
+
+
+def build_graph(inp: SchedulerInput, jobs: int = 1) -> PairGraph:
+    """Optimize every unordered pair and assemble the weighted pair graph.
+
+    ``jobs`` keeps the reference's meaning (worker threads) for plugin models;
+    the FNN path is one GPU sweep regardless.
+    """
+    weights = estimator.fnn_weights_of(inp.model)
+    if weights is not None:
+        return build_graph_gpu(inp.queue, inp.space, weights)
+    n = len(inp.queue)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+
+    def edge(pair):
+        return decide_pair(inp.model, inp.queue[pair[0]], inp.queue[pair[1]], inp.space)
+
+    if jobs > 1:
+        with ThreadPoolExecutor(max_workers=jobs) as pool:
+            decisions = list(pool.map(edge, pairs))
+    else:
+        decisions = [edge(p) for p in pairs]
+    w = np.zeros((n, n))
+    payload = {}
+    for (i, j), d in zip(pairs, decisions):
+        w[i, j] = w[j, i] = d.winning_time
+        payload[(i, j)] = d
+    return PairGraph(w, payload)
+
+
+def emit_schedule(inp: SchedulerInput, graph: PairGraph, matched) -> Schedule:
+    """Job sets from matched pairs; solo-flagged pairs split in edge order (scheduler.py:90-107)."""
+    sets, configs, flags = [], [], []
+    for i, j in matched:
+        d = graph.decisions[(i, j)]
+        if d.corun_chosen:
+            sets.append(JobSet((inp.queue[i], inp.queue[j])))
+            configs.append((d.corun_config,))
+            flags.append(True)
+        else:
+            for k, hc in zip((i, j), d.solo_configs):
+                sets.append(JobSet((inp.queue[k],)))
+                configs.append((hc,))
+                flags.append(False)
+    out = Schedule(tuple(sets), tuple(configs), tuple(flags))
+    out.validate_against(inp.queue, inp.space)
+    return out
+
+
+def schedule(inp: SchedulerInput, jobs: int = 1) -> Schedule:
+    """Dispatch plan for the queue: sweep, match, emit."""
+    graph = build_graph(inp, jobs=jobs)
+    return emit_schedule(inp, graph, min_weight_perfect_matching(graph))
+
+
+def set_time(model, js: JobSet, configs: Sequence, corun: bool, space: ConfigSpace) -> float:
+    """Predicted dispatch time of one emitted set (scheduler.py:110-116)."""
+    if corun:
+        return estimator.corun_time(model, js, configs[0], space)
+    hc = configs[0]
+    return estimator.solo_app_time(model, js.jobs[0], hc.cpu_cap, hc.gpu_cap, space)
+
+
+def predicted_makespan(sched: Schedule, model, space: ConfigSpace) -> float:
+    return sum(set_time(model, js, cs, fl, space)
+               for js, cs, fl in zip(sched.job_sets, sched.configs, sched.corun_flags))
+
+
+def schedule_to_json(sched: Schedule, model, space: ConfigSpace) -> dict:
+    sets = [{"jobs": [job.job_id for job in js.jobs], "corun": bool(fl),
+             "configs": [hc.to_json() for hc in cs],
+             "predicted_s": set_time(model, js, cs, fl, space)}
+            for js, cs, fl in zip(sched.job_sets, sched.configs, sched.corun_flags)]
+    return {"p_total_w": space.p_total, "sets": sets,
+            "total_predicted_s": predicted_makespan(sched, model, space)}
+
+
+def write_schedule_json(sched: Schedule, model, space: ConfigSpace, path) -> None:
+    with open(path, "w") as fh:
+        json.dump(schedule_to_json(sched, model, space), fh, indent=2, sort_keys=True)
+        fh.write("\n")

@@ -1,0 +1,133 @@
+"""Batched pair x knob sweep: the entry point behind hwopt/scheduler for FNN models.
+
+``sweep_pairs(weights, jobs, spaces)`` runs the fused GPU pipeline once over
+every unordered pair of ``jobs`` (row-major i < j, scheduler.py:61) for up to 8
+budgets and returns a ``SweepResult`` of host arrays.  ``hwopt.decide_pair``
+is the 2-job special case; ``scheduler.build_graph`` wraps the result in a
+``PairGraph`` with a lazy ``decisions`` mapping.
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from .core import ConfigSpace, JobProfile, ValidationError
+from .device import DEFAULT_REL_EPS, SweepPlan, require_cuda, to_device_inputs
+from .grid import KnobGrid
+
+_PLAN_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_PLAN_CACHE_SIZE = 8
+_GRID_CACHE: "OrderedDict[tuple, KnobGrid]" = OrderedDict()
+
+
+def knob_grid(spaces: Sequence[ConfigSpace]) -> KnobGrid:
+    key = tuple(spaces)
+    g = _GRID_CACHE.get(key)
+    if g is None:
+        g = KnobGrid(key)
+        _GRID_CACHE[key] = g
+        while len(_GRID_CACHE) > 32:
+            _GRID_CACHE.popitem(last=False)
+    return g
+
+
+def plan_for(weights, spaces: Sequence[ConfigSpace], n: int, pair_begin: int = 0,
+             pair_end: Optional[int] = None, with_matrix: bool = True,
+             rel_eps: float = DEFAULT_REL_EPS) -> SweepPlan:
+    """A cached SweepPlan (buffers are reused across calls of the same shape)."""
+    dev = require_cuda()
+    key = (id(weights), tuple(spaces), n, pair_begin, pair_end, with_matrix, rel_eps, str(dev))
+    hit = _PLAN_CACHE.get(key)
+    if hit is not None and hit[0] is weights:
+        _PLAN_CACHE.move_to_end(key)
+        return hit[1]
+    plan = SweepPlan(weights, knob_grid(spaces), n, pair_begin, pair_end, dev,
+                     with_matrix=with_matrix, rel_eps=rel_eps)
+    _PLAN_CACHE[key] = (weights, plan)          # holds `weights` so its id stays unique
+    while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+        _PLAN_CACHE.popitem(last=False)
+    return plan
+
+
+@dataclass
+class SweepResult:
+    """Host copies of one sweep.  Budget-major arrays: [l, p] / [l, app]."""
+
+    n: int
+    grid: KnobGrid
+    pair_begin: int
+    pair_end: int
+    corun_grid_index: np.ndarray     # (L, P) int32, union-grid index of the best config
+    corun_time: np.ndarray           # (L, P) float64
+    corun_chosen: np.ndarray         # (L, P) bool
+    weight: np.ndarray               # (L, P) float64 = winning_time
+    solo_time: np.ndarray            # (L, N) float64, best exclusive time per app
+    solo_split: np.ndarray           # (L, N) int32, index into grid.solo_splits[l]
+    solo_clamps: np.ndarray          # (L, N) int32, floored solo predictions per app
+    clamps: np.ndarray               # (L,) floor clamps as the reference would count them
+    queue_len: int                   # (pair, budget)s re-scanned exactly in fp64
+    screen_error: float              # largest fp32-screen vs fp64 relative gap seen
+    matrix: Optional[np.ndarray] = field(default=None)   # (L, N, N) symmetric weights
+
+    def corun_local_index(self, l: int) -> np.ndarray:
+        """Best config as an index into budget l's own enumerate_corun_configs list."""
+        return self.grid.local_index[l][self.corun_grid_index[l]]
+
+    def solo_pair_time(self, l: int, i, j):
+        """(0.0 + t_i) + t_j exactly as estimator.solorun_time sums (estimator.py:168-178)."""
+        st = self.solo_time[l]
+        return (0.0 + st[i]) + st[j]
+
+
+def _inputs(jobs: Sequence[JobProfile]):
+    feats = np.stack([np.asarray(j.features, dtype=np.float64) for j in jobs])
+    bt = np.array([float(j.base_time) for j in jobs], dtype=np.float64)
+    return feats, bt
+
+
+def run_plan(plan: SweepPlan, features: np.ndarray, base_time: np.ndarray,
+             with_matrix: bool = True) -> SweepResult:
+    d_f, d_b = to_device_inputs(features, base_time, plan.device)
+    with torch.cuda.device(plan.device):
+        plan.launch(d_f, d_b)
+        c = plan.read_counters()            # synchronizes the stream
+        P = plan.P
+        res = SweepResult(
+            n=plan.n, grid=plan.grid, pair_begin=plan.pair_begin, pair_end=plan.pair_end,
+            corun_grid_index=plan.corun_grid_index[:, :P].cpu().numpy(),
+            corun_time=plan.corun_time[:, :P].cpu().numpy(),
+            corun_chosen=plan.corun_chosen[:, :P].cpu().numpy().astype(bool),
+            weight=plan.weight[:, :P].cpu().numpy(),
+            solo_time=plan.solo_time.cpu().numpy(),
+            solo_split=plan.solo_split.cpu().numpy(),
+            solo_clamps=plan.solo_clamps.cpu().numpy(),
+            clamps=c.clamps, queue_len=c.queue_len, screen_error=c.screen_error,
+            matrix=plan.matrix.cpu().numpy() if (with_matrix and plan.matrix is not None) else None)
+    if res.screen_error > 0.25 * plan.rel_eps:
+        raise RuntimeError(f"fp32 screen error {res.screen_error:.3g} is too close to rel_eps "
+                           f"{plan.rel_eps:.3g}; argmin parity is no longer guaranteed")
+    return res
+
+
+def sweep_pairs(weights, jobs: Sequence[JobProfile], spaces, pair_begin: int = 0,
+                pair_end: Optional[int] = None, with_matrix: bool = True,
+                need_corun: bool = True, need_solo: bool = True) -> SweepResult:
+    """Evaluate every (pair, config) of `jobs` for each budget in `spaces` on the GPU.
+
+    Raises the reference's ValidationErrors for an empty co-run space
+    (hwopt.py:62-64) / unreachable budget (estimator.py:165-167) when the
+    corresponding part of the result is needed."""
+    if isinstance(spaces, ConfigSpace):
+        spaces = (spaces,)
+    jobs = list(jobs)
+    if len(jobs) < 2:
+        raise ValidationError("a sweep needs at least two jobs")
+    knob_grid(tuple(spaces)).check_nonempty(corun=need_corun, solo=need_solo)
+    feats, bt = _inputs(jobs)
+    plan = plan_for(weights, tuple(spaces), len(jobs), pair_begin, pair_end, with_matrix)
+    return run_plan(plan, feats, bt, with_matrix)

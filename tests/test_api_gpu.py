@@ -1,0 +1,98 @@
+"""The drop-in API (hwopt / scheduler / estimator) against the reference fixtures, on GPU."""
+
+import numpy as np
+import pytest
+
+from conftest import pair_index, space_for, workload
+import paper_2405_03831_b200 as cs
+from paper_2405_03831_b200 import core, estimator, synth
+
+pytestmark = pytest.mark.gpu
+REL = 1e-12
+
+
+def _hc(t):
+    return core.HardwareConfig(tuple(t[0]), tuple(t[1]), t[2], t[3])
+
+
+def test_decide_pair_matches_reference_samples(weights, samples):
+    entry = samples["n4096_400"]
+    jobs = synth.generate_workload(0, synth.mixed_archetypes(4096))
+    space = space_for(entry)
+    configs = core.enumerate_corun_configs(space)
+    splits = core.enumerate_solo_splits(space)
+    for row in entry["pairs"][:25]:
+        d = cs.decide_pair(weights, jobs[row["i"]], jobs[row["j"]], space)
+        assert d.corun_config == configs[row["corun_index"]]
+        assert d.corun_chosen == row["corun_chosen"]
+        assert abs(d.corun_time_s - row["corun_time_s"]) <= REL * row["corun_time_s"]
+        assert abs(d.solo_time_s - row["solo_time_s"]) <= REL * row["solo_time_s"]
+        assert [(hc.cpu_cap, hc.gpu_cap) for hc in d.solo_configs] == \
+            [splits[k] for k in row["solo_split_index"]]
+        hc, t = cs.optimize_corun(weights, jobs[row["i"]], jobs[row["j"]], space)
+        assert hc == d.corun_config and t == d.corun_time_s
+        s1, s2, st = cs.optimize_solo_pair(weights, jobs[row["i"]], jobs[row["j"]], space)
+        assert (s1, s2) == d.solo_configs and st == d.solo_time_s
+
+
+@pytest.mark.parametrize("budget", ["400", "350"])
+def test_build_graph_and_schedule_match_reference(weights, paper20, budget):
+    sp = paper20["spaces"][budget]
+    jobs = synth.generate_workload(0, synth.mixed_archetypes(20))
+    space = core.default_space(float(budget))
+    inp = cs.SchedulerInput(tuple(jobs), space, core.SchedulingParams(window=20), weights)
+    estimator.clamp_stats.reset()
+    graph = cs.build_graph(inp, jobs=4)
+    assert estimator.clamp_stats.count == sp["clamp_count_build_graph"]
+    assert len(graph.decisions) == 190
+    assert list(graph.decisions.keys()) == [(p["i"], p["j"]) for p in sp["pairs"]]
+    for p in sp["pairs"]:
+        d = graph.decisions[(p["i"], p["j"])]
+        assert d.corun_config == _hc(p["corun_config"])
+        assert d.corun_chosen == p["corun_chosen"]
+        assert abs(d.winning_time - p["winning_time"]) <= REL * p["winning_time"]
+        assert graph.weights[p["i"], p["j"]] == d.winning_time
+    matched = cs.min_weight_perfect_matching(graph)
+    assert [list(m) for m in matched] == sp["matching"]
+    assert abs(cs.matching_weight(graph, matched) - sp["matching_weight"]) <= REL * sp["matching_weight"]
+    sched = cs.schedule(inp)
+    ref = sp["schedule"]
+    assert [[j.job_id for j in js.jobs] for js in sched.job_sets] == ref["job_sets"]
+    assert list(sched.corun_flags) == ref["corun_flags"]
+    assert [[_hc(t) for t in cfgs] for cfgs in ref["configs"]] == [list(c) for c in sched.configs]
+    mk = cs.predicted_makespan(sched, weights, space)
+    assert abs(mk - ref["predicted_makespan"]) <= 1e-12 * ref["predicted_makespan"]
+
+
+def test_full_256_schedule_matches_reference_matching(weights, n256):
+    jobs = synth.generate_workload(0, synth.mixed_archetypes(256))
+    inp = cs.SchedulerInput(tuple(jobs), core.default_space(400.0),
+                            core.SchedulingParams(window=256), weights)
+    graph = cs.build_graph(inp)
+    matched = cs.min_weight_perfect_matching(graph)
+    assert np.array_equal(np.array(matched), n256["matching"])
+    assert abs(cs.matching_weight(graph, matched) - float(n256["matching_weight"])) <= \
+        1e-12 * float(n256["matching_weight"])
+
+
+def test_empty_search_spaces_raise_like_the_reference(weights):
+    jobs = synth.generate_workload(0, synth.mixed_archetypes(2))
+    with pytest.raises(core.ValidationError, match="no co-run configs"):
+        cs.optimize_corun(weights, jobs[0], jobs[1], core.default_space(300.0))
+    # 300 W has solo splits but no co-run level: the solo optimizer still works
+    s1, s2, t = cs.optimize_solo_pair(weights, jobs[0], jobs[1], core.default_space(300.0))
+    assert s1.cap_sum == 300.0 and t > 0
+    with pytest.raises(core.ValidationError, match="unreachable"):
+        cs.decide_pair(weights, jobs[0], jobs[1], core.default_space(360.0))
+    hc, t = cs.optimize_corun(weights, jobs[0], jobs[1], core.default_space(360.0))
+    assert hc.cap_sum == 350.0
+
+
+def test_scalar_predictions_match_sweep(weights):
+    jobs = synth.generate_workload(0, synth.mixed_archetypes(6))
+    space = core.default_space(400.0)
+    d = cs.decide_pair(weights, jobs[2], jobs[5], space)
+    t = cs.corun_time(weights, core.JobSet((jobs[2], jobs[5])), d.corun_config, space)
+    assert abs(t - d.corun_time_s) <= REL * t
+    total, splits = cs.solorun_time(weights, core.JobSet((jobs[2], jobs[5])), space)
+    assert abs(total - d.solo_time_s) <= REL * total

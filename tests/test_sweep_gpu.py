@@ -1,0 +1,190 @@
+"""GPU parity: the sm_100a sweep against the CPU oracle and the reference fixtures.
+
+Bar: argmin config index, co-run flag and solo split EXACT; every fp64 output
+(co-run time, solo time, weight) bit-identical to the oracle (same fma order)
+and within 1e-12 relative of the reference (BLAS summation order).  The fp32
+screen is allowed no influence on results: pairs whose runner-up lies within
+rel_eps = 1e-4 of the minimum are re-scanned in fp64 (cs_resolve).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import pair_index, space_for, workload
+from paper_2405_03831_b200 import core, fnn
+from paper_2405_03831_b200.grid import KnobGrid
+from paper_2405_03831_b200.sweep import sweep_pairs
+from paper_2405_03831_b200 import synth
+
+pytestmark = pytest.mark.gpu
+REL = 1e-12
+
+
+def _jobs(n, seed=0):
+    return synth.generate_workload(seed, synth.mixed_archetypes(n))
+
+
+def _assert_same_as_oracle(res, ref, l=0):
+    assert np.array_equal(res.corun_grid_index[l], ref["corun_grid_index"][l])
+    assert np.array_equal(res.corun_chosen[l], ref["corun_chosen"][l])
+    assert np.array_equal(res.corun_time[l], ref["corun_time"][l])      # bit-identical
+    assert np.array_equal(res.weight[l], ref["weight"][l])
+    assert np.array_equal(res.solo_time[l], ref["solo_time"][l])
+    assert np.array_equal(res.solo_split[l], ref["solo_split"][l])
+
+
+@pytest.mark.parametrize("budget", ["400", "350"])
+def test_paper20_bit_exact(weights, paper20, budget):
+    sp = paper20["spaces"][budget]
+    jobs = _jobs(20)
+    space = core.default_space(float(budget))
+    res = sweep_pairs(weights, jobs, space)
+    F, T = workload(20)
+    ref = oracle.sweep(weights, F, T, KnobGrid([space]))
+    _assert_same_as_oracle(res, ref)
+    rows = sp["pairs"]
+    assert res.corun_local_index(0).tolist() == [p["corun_index"] for p in rows]
+    assert np.max(np.abs(res.weight[0] - [p["winning_time"] for p in rows]) /
+                  np.array([p["winning_time"] for p in rows])) <= REL
+    M = res.matrix[0]
+    assert np.array_equal(M, M.T) and np.all(np.diag(M) == 0)
+    for p in rows:
+        assert M[p["i"], p["j"]] == res.weight[0, pair_index(20, p["i"], p["j"])]
+    total_clamps = int(res.clamps[0])
+    assert total_clamps == sp["clamp_count_build_graph"]
+    assert res.screen_error < 1e-5
+
+
+def test_full_reference_graph_256(weights, n256):
+    res = sweep_pairs(weights, _jobs(256), core.default_space(400.0))
+    assert np.array_equal(res.corun_local_index(0), n256["corun_index"])
+    assert np.array_equal(res.corun_chosen[0], n256["corun_chosen"].astype(bool))
+    assert np.max(np.abs(res.corun_time[0] - n256["corun_time"]) / n256["corun_time"]) <= REL
+    assert np.max(np.abs(res.weight[0] - n256["winning_time"]) / n256["winning_time"]) <= REL
+    F, T = workload(256)
+    _assert_same_as_oracle(res, oracle.sweep(weights, F, T, KnobGrid([core.default_space(400.0)])))
+
+
+def test_five_budget_sweep_1024_shards(weights):
+    n = 1024
+    spaces = [core.ConfigSpace(p_total=p, cap_sum_levels=(300, 325, 350, 375, 400))
+              for p in (300.0, 325.0, 350.0, 375.0, 400.0)]
+    grid = KnobGrid(spaces)
+    F, T = workload(n)
+    jobs = _jobs(n)
+    P = n * (n - 1) // 2
+    for b, e in ((0, 6000), (P // 2 - 3000, P // 2 + 3000), (P - 6000, P)):
+        res = sweep_pairs(weights, jobs, spaces, b, e, with_matrix=False)
+        ref = oracle.sweep(weights, F, T, grid, b, e)
+        for l in range(5):
+            _assert_same_as_oracle(res, ref, l)
+
+
+@pytest.mark.parametrize("key", ["n4096_400", "n4096_350", "n4096_fine400"])
+def test_full_4096_sweep_against_reference_samples(weights, samples, key):
+    entry = samples[key]
+    n = entry["n"]
+    space = space_for(entry)
+    res = sweep_pairs(weights, _jobs(n), space, with_matrix=False)
+    local = res.corun_local_index(0)
+    for row in entry["pairs"]:
+        p = pair_index(n, row["i"], row["j"])
+        assert local[p] == row["corun_index"]
+        assert res.corun_chosen[0, p] == row["corun_chosen"]
+        assert abs(res.corun_time[0, p] - row["corun_time_s"]) <= REL * row["corun_time_s"]
+        assert abs(res.weight[0, p] - row["winning_time"]) <= REL * row["winning_time"]
+        assert [res.solo_split[0, row["i"]], res.solo_split[0, row["j"]]] == row["solo_split_index"]
+    # size-independent properties over all 8.4M pairs
+    iu, ju = np.triu_indices(n, 1)
+    solo = (0.0 + res.solo_time[0][iu]) + res.solo_time[0][ju]
+    assert np.array_equal(res.corun_chosen[0], res.corun_time[0] <= solo)
+    assert np.array_equal(res.weight[0], np.where(res.corun_chosen[0], res.corun_time[0], solo))
+    assert np.all(local >= 0) and np.all(local < res.grid.n_configs[0])
+    assert res.screen_error < 1e-5
+    assert res.queue_len < 0.05 * len(local)
+    # an oracle shard at full size, bit-exact
+    F, T = workload(n)
+    b = len(local) // 3
+    ref = oracle.sweep(weights, F, T, res.grid, b, b + 4000)
+    assert np.array_equal(res.corun_grid_index[0, b:b + 4000], ref["corun_grid_index"][0])
+    assert np.array_equal(res.weight[0, b:b + 4000], ref["weight"][0])
+
+
+def _zero_weights(bounds):
+    z = np.zeros
+    return fnn.NetworkWeights(z((18, 40)), z(18), z((18, 18)), z(18), z((1, 18)), z(1), bounds)
+
+
+def test_degenerate_zero_network_ties_and_clamps(weights):
+    # every prediction floors to 0.5: all configs tie -> first index (hwopt.py:59),
+    # co-run 0.5*max(T) <= solo 0.5*(Ti+Tj) -> co-run chosen; every prediction clamps
+    zw = _zero_weights(weights.feature_bounds)
+    n = 64
+    jobs = _jobs(n, 2)
+    space = core.default_space(400.0)
+    res = sweep_pairs(zw, jobs, space)
+    T = np.array([j.base_time for j in jobs])
+    iu, ju = np.triu_indices(n, 1)
+    assert np.all(res.corun_local_index(0) == 0)
+    assert np.array_equal(res.corun_time[0], 0.5 * np.maximum(T[iu], T[ju]))
+    assert np.all(res.corun_chosen[0])
+    assert np.all(res.solo_split[0] == 0)
+    P, C, S = len(iu), 100, 5
+    assert int(res.clamps[0]) == P * (2 * C + 2 * S)
+    assert res.queue_len == P           # every pair is an exact tie -> fp64 re-scan
+
+
+def test_shards_compose_to_full(weights):
+    jobs = _jobs(300, 1)
+    space = core.default_space(350.0)
+    full = sweep_pairs(weights, jobs, space, with_matrix=False)
+    P = 300 * 299 // 2
+    cuts = [0, 1, 777, P // 2, P - 5, P]
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        part = sweep_pairs(weights, jobs, space, b, e, with_matrix=False)
+        assert np.array_equal(part.corun_grid_index[0], full.corun_grid_index[0, b:e])
+        assert np.array_equal(part.weight[0], full.weight[0, b:e])
+
+
+def test_host_abi_matches_device_path(weights):
+    from paper_2405_03831_b200.host_abi import build_graph_host
+    jobs = _jobs(128, 4)
+    spaces = [core.default_space(400.0), core.default_space(350.0)]
+    dev = sweep_pairs(weights, jobs, spaces)
+    F, T = workload(128, 4)
+    host = build_graph_host(weights, KnobGrid(spaces), F, T)
+    for l in range(2):
+        assert np.array_equal(host["weights"][l], dev.matrix[l])
+        assert np.array_equal(host["corun_grid_index"][l], dev.corun_grid_index[l])
+        assert np.array_equal(host["corun_time"][l], dev.corun_time[l])
+    assert np.array_equal(host["clamps"].astype(np.int64), dev.clamps)
+
+
+def test_forward_rows_matches_oracle(weights):
+    from paper_2405_03831_b200 import fnn as f
+    rng = np.random.default_rng(5)
+    X = rng.uniform(0, 1, size=(257, 40))
+    y = f.forward_batch(weights, X)
+    for k in range(0, 257, 16):
+        x = X[k]
+        want = oracle.predict(weights, x[4:22] * weights.feature_bounds[:18],
+                              x[22:] * weights.feature_bounds[18:], x[:4])
+        assert abs(y[k] - want) <= 1e-12 * max(1.0, abs(want))
+    assert f.forward(weights, X[3]) == y[3]
+
+
+def test_no_cpu_fallback_when_extension_missing(monkeypatch, weights):
+    from paper_2405_03831_b200 import _native
+    monkeypatch.setattr(_native, "SWEEP_LIB", "/nonexistent/libcosched_b200.so")
+    monkeypatch.setattr(_native, "_libs", {})
+    from paper_2405_03831_b200.device import SweepPlan
+    with pytest.raises(_native.NativeLibraryError):
+        SweepPlan(weights, KnobGrid([core.default_space()]), 8)
+
+
+def test_cuda_is_the_path():
+    assert torch.cuda.is_available()
+    cap = torch.cuda.get_device_capability(0)
+    assert cap[0] >= 10, f"expected a Blackwell (sm_100) device, got sm_{cap[0]}{cap[1]}"
