@@ -1,0 +1,98 @@
+"""Native matcher (csrc/matching.cpp) vs the reference's matcher fixtures and brute force. CPU."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2405_03831_b200 import matcher
+from paper_2405_03831_b200.core import ValidationError
+
+
+def random_graph(n, seed):
+    """Same generator as tests/golden/make_golden.py."""
+    rng = np.random.default_rng([seed, n, 7])
+    w = np.triu(rng.uniform(10.0, 100.0, size=(n, n)), 1)
+    return w + w.T
+
+
+with open(os.path.join(GOLDEN, "matching.json")) as fh:
+    CASES = json.load(fh)
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c['n']}s{c['seed']}")
+def test_matches_reference_matcher(case):
+    W = np.array(case["weights"]) if case.get("integer_ties") else random_graph(case["n"], case["seed"])
+    g = matcher.PairGraph(W)
+    pairs = matcher.min_weight_perfect_matching(g)
+    total = matcher.matching_weight(g, pairs)
+    assert abs(total - case["weight"]) <= 1e-12 * case["weight"]
+    if not case.get("integer_ties"):       # continuous weights: unique optimum
+        assert [list(p) for p in pairs] == case["pairs"]
+    if "brute_force_weight" in case:
+        assert abs(total - case["brute_force_weight"]) <= 1e-12 * case["brute_force_weight"]
+
+
+@pytest.mark.parametrize("n", [2, 4, 6, 8, 10])
+def test_against_brute_force_many_seeds(n):
+    for seed in range(25):
+        rng = np.random.default_rng([seed, n, 11])
+        w = np.triu(rng.integers(0, 6, size=(n, n)).astype(float), 1)   # heavy ties
+        g = matcher.PairGraph(w + w.T)
+        pairs = matcher.min_weight_perfect_matching(g)
+        assert sorted(v for p in pairs for v in p) == list(range(n))
+        _, best = matcher.brute_force_matching(g)
+        assert matcher.matching_weight(g, pairs) == best
+
+
+def test_dual_certificate_random_256():
+    """Optimality without an oracle: a perfect matching M is minimum iff no
+    alternating cycle improves it; spot-check with 2-opt swaps on every matched
+    pair couple (a necessary condition, exhaustive over O(n^2) swaps)."""
+    W = random_graph(256, 42)
+    g = matcher.PairGraph(W)
+    pairs = matcher.min_weight_perfect_matching(g)
+    P = np.array(pairs)
+    a, b = P[:, 0], P[:, 1]
+    base = W[a, b]
+    for k in range(len(P)):
+        cur = base[k] + base
+        alt1 = W[a[k], a] + W[b[k], b]
+        alt2 = W[a[k], b] + W[b[k], a]
+        alt1[k] = alt2[k] = np.inf
+        assert np.all(alt1 >= cur - 1e-9) and np.all(alt2 >= cur - 1e-9)
+
+
+def test_max_weight_matching_general():
+    w = np.array([[0, 5, 1, 0], [5, 0, 9, 0], [1, 9, 0, 2], [0, 0, 2, 0]], dtype=float)
+    mate = matcher.max_weight_matching(w)
+    # best: (0,1)+(2,3) = 7 vs (1,2) = 9 -> (1,2) alone or (1,2)+(0,3=0)
+    assert mate[1] == 2 and mate[2] == 1
+
+
+def test_pairgraph_validation():
+    with pytest.raises(ValidationError, match="square"):
+        matcher.PairGraph(np.zeros((2, 3)))
+    with pytest.raises(ValidationError, match="even"):
+        matcher.PairGraph(np.zeros((3, 3)))
+    with pytest.raises(ValidationError, match="symmetric"):
+        matcher.PairGraph(np.array([[0, 1.0], [2.0, 0]]))
+    with pytest.raises(ValidationError, match=">= 0"):
+        matcher.PairGraph(np.array([[0, -1.0], [-1.0, 0]]))
+    g = matcher.PairGraph(np.array([[7.0, 1.0], [1.0, 9.0]]))
+    assert g.weights[0, 0] == 0 and not g.weights.flags.writeable
+
+
+def test_brute_force_limit():
+    with pytest.raises(ValidationError):
+        matcher.brute_force_matching(matcher.PairGraph(np.ones((14, 14)) - np.eye(14)))
+
+
+def test_graph_csv(tmp_path):
+    g = matcher.PairGraph(random_graph(4, 0))
+    p = tmp_path / "g.csv"
+    matcher.graph_to_csv(g, p)
+    rows = p.read_text().splitlines()
+    assert rows[0] == "i,j,weight,corun_flag" and len(rows) == 7
