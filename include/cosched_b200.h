@@ -60,6 +60,14 @@ enum {
     CS_ERR_WORKSPACE = -5     /* workspace smaller than required       -> ValueError      */
 };
 
+/* Screen kernels of cs_pair_sweep_ex (results are identical: both feed the same
+ * exact fp64 re-evaluation / re-scan). */
+enum {
+    CS_KERNEL_AUTO = 0,       /* tcgen05 on sm_100a                                       */
+    CS_KERNEL_TCGEN05 = 1,    /* layer 2 on the tensor cores: fp16 3-term split, fp32 acc */
+    CS_KERNEL_SIMT = 2        /* layer 2 as fp32 FFMA with W2 in the parameter bank       */
+};
+
 /* NetworkWeights (fnn.py:42-68), HOST fp64, row-major exactly as the
  * reference's JSON v1 document (fnn.py:311-324).  Copied by value into the
  * kernel parameter bank at each launch. */
@@ -97,7 +105,7 @@ typedef struct {
 /* Device tables carved from one caller buffer by cs_tables_bind. */
 typedef struct {
     int32_t n_apps, n_grid, n_solo;
-    double *net64;                /* fp64 copy of w2|b2|w_out|b_out for the exact path */
+    uint16_t *w2_tile;            /* fp16 [W2hi|W2hi|W2lo|b2] B operand of the tcgen05 screen */
     float *app_a32, *app_b32;     /* N x 20 (18 + pad): primary / co-runner partials */
     double *app_a64, *app_b64;    /* N x 18 */
     float *knob1_32, *knob2_32;   /* G x 20, b1 folded */
@@ -131,8 +139,8 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
 int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
                     const cs_grid *d_grid, const cs_tables *tables, void *stream);
 
-int cs_solo(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
-            cs_solo_out out, void *stream);
+int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+            const double *d_base_time, cs_solo_out out, void *stream);
 
 /* `net` (host) is passed again because the fp32 screen keeps W2 in the kernel
  * parameter bank.  Screens every (pair, config) of the shard in fp32, keeps per (pair, budget)
@@ -153,10 +161,17 @@ int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid 
                   int64_t pair_end, double rel_eps, cs_pair_out out, int64_t *d_queue,
                   uint32_t *d_queue_count, unsigned long long *d_clamps, void *stream);
 
-int cs_resolve(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
-               const double *d_solo_time, int64_t pair_begin, int64_t pair_end,
-               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
-               void *stream);
+/* cs_pair_sweep with an explicit screen kernel (CS_KERNEL_*). */
+int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, int kernel_kind, void *stream);
+
+int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+               const double *d_base_time, const double *d_solo_time, int64_t pair_begin,
+               int64_t pair_end, cs_pair_out out, const int64_t *d_queue,
+               const uint32_t *d_queue_count, void *stream);
 
 /* W[i*N+j] = W[j*N+i] = weight of budget `budget`; the caller zeroes W. */
 int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,

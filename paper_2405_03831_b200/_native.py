@@ -20,6 +20,7 @@ SWEEP_LIB = os.path.join(_HERE, "libcosched_b200.so")
 MATCH_LIB = os.path.join(_HERE, "libcosched_match.so")
 
 MAX_BUDGETS = 8
+KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT = 0, 1, 2
 _lock = threading.Lock()
 _libs: dict = {}
 
@@ -53,7 +54,7 @@ class CsGrid(ctypes.Structure):
 
 class CsTables(ctypes.Structure):
     _fields_ = [("n_apps", ctypes.c_int32), ("n_grid", ctypes.c_int32), ("n_solo", ctypes.c_int32),
-                ("net64", c_double_p), ("app_a32", c_float_p), ("app_b32", c_float_p),
+                ("w2_tile", ctypes.c_void_p), ("app_a32", c_float_p), ("app_b32", c_float_p),
                 ("app_a64", c_double_p), ("app_b64", c_double_p),
                 ("knob1_32", c_float_p), ("knob2_32", c_float_p),
                 ("knob1_64", c_double_p), ("knob2_64", c_double_p), ("solo64", c_double_p)]
@@ -78,14 +79,21 @@ SWEEP_SYMBOLS = {
     "cs_build_tables": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_int32,
                                        ctypes.POINTER(CsGrid), ctypes.POINTER(CsTables),
                                        ctypes.c_void_p]),
-    "cs_solo": (ctypes.c_int, [ctypes.POINTER(CsTables), ctypes.POINTER(CsGrid), ctypes.c_void_p,
-                               CsSoloOut, ctypes.c_void_p]),
+    "cs_solo": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                               ctypes.POINTER(CsGrid), ctypes.c_void_p, CsSoloOut, ctypes.c_void_p]),
     "cs_pair_sweep": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
                                      ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_double, CsPairOut, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
-    "cs_resolve": (ctypes.c_int, [ctypes.POINTER(CsTables), ctypes.POINTER(CsGrid),
+    "cs_pair_sweep_ex": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                                        ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_double, CsPairOut, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_void_p]),
+    "cs_resolve": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                                  ctypes.POINTER(CsGrid),
                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_int64, CsPairOut, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p]),

@@ -18,6 +18,7 @@
 // so fp64 outputs are bit-identical to the C restatement of the reference.
 #include "cosched_b200.h"
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -32,7 +33,7 @@ constexpr int NF = CS_NUM_FEATURES;
 constexpr int HD = CS_HIDDEN;
 constexpr int IN = CS_INPUT_DIM;
 constexpr int ROW32 = 20;                  // fp32 table row: 18 + 2 pad (80 B, float4-aligned)
-constexpr int NET64_LEN = HD * HD + HD + HD + 1;  // w2 | b2 | w_out | b_out
+constexpr int W2_TILE_ELEMS = 32 * 64;     // fp16 B tile of the tcgen05 screen
 constexpr double FLOOR = 0.5;              // estimator.py:33
 constexpr int kSweepThreads = 128;
 
@@ -100,41 +101,110 @@ __device__ __forceinline__ void pair_of(int64_t p, int n, int &i, int &j) {
 }
 
 // ---- fp64 exact path (mirrors orc_head in oracle/cosched_oracle.c) --------
-// net64 layout: w2[324] | b2[18] | wo[18] | bo
-__device__ __forceinline__ double head64(const double *__restrict__ net, const double *z) {
-    double h1[HD];
+// The fp64 head weights ride in the kernel parameter bank (DFMA constant
+// operands, no loads).  Loop order k-outer / o-inner keeps 18 independent
+// accumulation chains in flight while every chain still sums over k in the
+// oracle's order, so results stay bit-identical to it.
+struct Head64P {
+    double w2[HD * HD];
+    double b2[HD];
+    double wo[HD];
+    double bo;
+};
+
+Head64P head64_from(const Net64P &n) {
+    Head64P h;
+    memcpy(h.w2, n.w2, sizeof(h.w2));
+    memcpy(h.b2, n.b2, sizeof(h.b2));
+    memcpy(h.wo, n.wo, sizeof(h.wo));
+    h.bo = n.bo;
+    return h;
+}
+
+__device__ __forceinline__ double head64c(const Head64P &net, const double (&z)[HD]) {
+    double acc[HD];
 #pragma unroll
-    for (int k = 0; k < HD; ++k) h1[k] = z[k] > 0.0 ? z[k] : 0.0;
-    double y = 0.0;
-#pragma unroll 3
-    for (int o = 0; o < HD; ++o) {
-        double acc = 0.0;
+    for (int o = 0; o < HD; ++o) acc[o] = 0.0;
 #pragma unroll
-        for (int k = 0; k < HD; ++k) acc = fma(h1[k], __ldg(net + o * HD + k), acc);
-        acc = acc + __ldg(net + HD * HD + o);
-        y = fma(acc > 0.0 ? acc : 0.0, __ldg(net + HD * HD + HD + o), y);
+    for (int k = 0; k < HD; ++k) {
+        const double hk = z[k] > 0.0 ? z[k] : 0.0;
+#pragma unroll
+        for (int o = 0; o < HD; ++o) acc[o] = fma(hk, net.w2[o * HD + k], acc[o]);
     }
-    y = y + __ldg(net + HD * HD + 2 * HD);
+    double y = 0.0;
+#pragma unroll
+    for (int o = 0; o < HD; ++o) {
+        const double a2 = acc[o] + net.b2[o];
+        y = fma(a2 > 0.0 ? a2 : 0.0, net.wo[o], y);
+    }
+    y = y + net.bo;
     return y > 0.0 ? y : 0.0;
 }
 
-// CoRunTime of one config for pair (i, j): max over members of floor(pred) x T.
-__device__ double corun64(const cs_tables &t, const double *__restrict__ base_time, int i, int j,
-                          int c) {
+// floor(pred) x T of one member of pair (self, other) under config c
+// (member 0: K1 / view hc, member 1: K2 / reversed partitions)
+__device__ __forceinline__ double member_time64(const cs_tables &t, const Head64P &net,
+                                                const double *__restrict__ base_time, int self,
+                                                int other, int c, int member) {
     double z[HD];
-    const double *ai = t.app_a64 + (size_t)i * HD, *bj = t.app_b64 + (size_t)j * HD;
-    const double *aj = t.app_a64 + (size_t)j * HD, *bi = t.app_b64 + (size_t)i * HD;
-    const double *k1 = t.knob1_64 + (size_t)c * HD, *k2 = t.knob2_64 + (size_t)c * HD;
+    const double *as = t.app_a64 + (size_t)self * HD, *bo = t.app_b64 + (size_t)other * HD;
+    const double *kk = (member ? t.knob2_64 : t.knob1_64) + (size_t)c * HD;
 #pragma unroll
-    for (int h = 0; h < HD; ++h) z[h] = (__ldg(ai + h) + __ldg(bj + h)) + __ldg(k1 + h);
-    double y1 = head64(t.net64, z);
-#pragma unroll
-    for (int h = 0; h < HD; ++h) z[h] = (__ldg(aj + h) + __ldg(bi + h)) + __ldg(k2 + h);
-    double y2 = head64(t.net64, z);
-    double t1 = (y1 < FLOOR ? FLOOR : y1) * __ldg(base_time + i);
-    double t2 = (y2 < FLOOR ? FLOOR : y2) * __ldg(base_time + j);
+    for (int h = 0; h < HD; ++h) z[h] = (__ldg(as + h) + __ldg(bo + h)) + __ldg(kk + h);
+    const double y = head64c(net, z);
+    return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
+}
+
+// CoRunTime of one config for pair (i, j): max over members (estimator.py:127-129)
+__device__ __forceinline__ double corun64(const cs_tables &t, const Head64P &net,
+                                          const double *__restrict__ base_time, int i, int j,
+                                          int c) {
+    const double t1 = member_time64(t, net, base_time, i, j, c, 0);
+    const double t2 = member_time64(t, net, base_time, j, i, c, 1);
     return t1 > t2 ? t1 : t2;
 }
+
+// ---- shared by both screens ----------------------------------------------
+struct SweepArgs {
+    cs_tables t;
+    GridP g;
+    const double *base_time, *solo_time;
+    const int32_t *solo_clamps;
+    int32_t n, log2s;
+    int64_t p_begin, P;
+    float eps;
+    cs_pair_out out;
+    int64_t *queue;
+    uint32_t *qcount;
+    unsigned long long *clamps;
+};
+
+__device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
+    float h[HD];
+#pragma unroll
+    for (int k = 0; k < HD; ++k) h[k] = fmaxf(z[k], 0.f);
+    float y = net.bo;
+#pragma unroll
+    for (int o = 0; o < HD; ++o) {
+        float acc = net.b2[o];
+#pragma unroll
+        for (int k = 0; k < HD; ++k) acc = fmaf(h[k], net.w2[o * HD + k], acc);
+        y = fmaf(fmaxf(acc, 0.f), net.wo[o], y);
+    }
+    return y;
+}
+
+__device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&r)[HD]) {
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    float4 v0 = __ldg(q), v1 = __ldg(q + 1), v2 = __ldg(q + 2), v3 = __ldg(q + 3), v4 = __ldg(q + 4);
+    r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
+    r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
+    r[8] = v2.x; r[9] = v2.y; r[10] = v2.z; r[11] = v2.w;
+    r[12] = v3.x; r[13] = v3.y; r[14] = v3.z; r[15] = v3.w;
+    r[16] = v4.x; r[17] = v4.y;
+}
+
+#include "tc_sweep.cuh"
 
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -142,14 +212,7 @@ __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v >
 __global__ void k_tables(const __grid_constant__ Net64P net, const double *__restrict__ feats,
                          int n, const GridP g, const cs_tables t) {
     int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid < NET64_LEN) {
-        double v;
-        if (tid < HD * HD) v = net.w2[tid];
-        else if (tid < HD * HD + HD) v = net.b2[tid - HD * HD];
-        else if (tid < HD * HD + 2 * HD) v = net.wo[tid - HD * HD - HD];
-        else v = net.bo;
-        t.net64[tid] = v;
-    }
+    if (tid < W2_TILE_ELEMS) write_b_tile(net, t.w2_tile, (int)tid);
     const int64_t rows = (int64_t)n + g.G + g.S;
     for (int64_t r = tid; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
         if (r < n) {
@@ -199,71 +262,43 @@ __global__ void k_tables(const __grid_constant__ Net64P net, const double *__res
 }
 
 // ---- k_solo: per (budget, app) best split, fp64 (estimator.py:160-180) ----
+// One warp per (budget, app); lane s evaluates split s (a budget has <= 32
+// splits: 17 on the 6.25 W grid), then a first-index argmin over the warp.
 __global__ void k_solo(const cs_tables t, const GridP g, const double *__restrict__ base_time,
-                       int n, cs_solo_out out) {
-    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= (int64_t)n * g.L) return;
-    const int l = (int)(tid / n), a = (int)(tid % n);
-    double z[HD];
-    double best = 0.0;
-    int arg = -1, clamps = 0;
-    const double T = base_time[a];
-    for (int s = g.solo_off[l]; s < g.solo_off[l + 1]; ++s) {
+                       int n, cs_solo_out out, const __grid_constant__ Head64P net) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= (int64_t)n * g.L) return;
+    const int l = (int)(w / n), a = (int)(w % n);
+    const int s0 = g.solo_off[l], ns = g.solo_off[l + 1] - s0;
+    double best = INFINITY;
+    int arg = INT_MAX, clamp = 0;
+    for (int s = lane; s < ns; s += 32) {
+        double z[HD];
 #pragma unroll
-        for (int h = 0; h < HD; ++h) z[h] = t.app_a64[(size_t)a * HD + h] + t.solo64[(size_t)s * HD + h];
-        double y = head64(t.net64, z);
-        if (y < FLOOR) { ++clamps; y = FLOOR; }
-        double tt = y * T;
-        if (arg < 0 || tt < best) { best = tt; arg = s - g.solo_off[l]; }
+        for (int h = 0; h < HD; ++h) z[h] = t.app_a64[(size_t)a * HD + h] + t.solo64[(size_t)(s0 + s) * HD + h];
+        double y = head64c(net, z);
+        if (y < FLOOR) { ++clamp; y = FLOOR; }
+        const double tt = y * base_time[a];
+        if (tt < best) { best = tt; arg = s; }
     }
-    out.solo_time[tid] = arg < 0 ? nan("") : best;
-    out.solo_split[tid] = arg;
-    if (out.solo_clamps) out.solo_clamps[tid] = clamps;
-}
-
-// ---- k_sweep: fp32 screen of (pair, config) + fused reductions ------------
-struct SweepArgs {
-    cs_tables t;
-    GridP g;
-    const double *base_time, *solo_time;
-    const int32_t *solo_clamps;
-    int32_t n, log2s;
-    int64_t p_begin, P;
-    float eps;
-    cs_pair_out out;
-    int64_t *queue;
-    uint32_t *qcount;
-    unsigned long long *clamps;
-};
-
-__device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
-    float h[HD];
-#pragma unroll
-    for (int k = 0; k < HD; ++k) h[k] = fmaxf(z[k], 0.f);
-    float y = net.bo;
-#pragma unroll
-    for (int o = 0; o < HD; ++o) {
-        float acc = net.b2[o];
-#pragma unroll
-        for (int k = 0; k < HD; ++k) acc = fmaf(h[k], net.w2[o * HD + k], acc);
-        y = fmaf(fmaxf(acc, 0.f), net.wo[o], y);
+    for (int off = 16; off; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, arg, off);
+        if (ob < best || (ob == best && oi < arg)) { best = ob; arg = oi; }
     }
-    return y;
-}
-
-__device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&r)[HD]) {
-    const float4 *q = reinterpret_cast<const float4 *>(p);
-    float4 v0 = __ldg(q), v1 = __ldg(q + 1), v2 = __ldg(q + 2), v3 = __ldg(q + 3), v4 = __ldg(q + 4);
-    r[0] = v0.x; r[1] = v0.y; r[2] = v0.z; r[3] = v0.w;
-    r[4] = v1.x; r[5] = v1.y; r[6] = v1.z; r[7] = v1.w;
-    r[8] = v2.x; r[9] = v2.y; r[10] = v2.z; r[11] = v2.w;
-    r[12] = v3.x; r[13] = v3.y; r[14] = v3.z; r[15] = v3.w;
-    r[16] = v4.x; r[17] = v4.y;
+    clamp = __reduce_add_sync(0xffffffffu, clamp);
+    if (lane == 0) {
+        out.solo_time[w] = arg == INT_MAX ? nan("") : best;
+        out.solo_split[w] = arg == INT_MAX ? -1 : arg;
+        if (out.solo_clamps) out.solo_clamps[w] = clamp;
+    }
 }
 
 template <int L>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
-                                                         const __grid_constant__ Net32P net) {
+                                                         const __grid_constant__ Net32P net,
+                                                         const __grid_constant__ Head64P net64) {
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int S = 1 << a.log2s;
     const int64_t pl = gt >> a.log2s;          // local pair index
@@ -343,7 +378,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
             continue;
         }
         const int c = idx[l];
-        const double co = corun64(a.t, a.base_time, i, j, c);
+        const double co = corun64(a.t, net64, a.base_time, i, j, c);
         const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
         const bool chosen = co <= solo;                       // hwopt.py:86
         a.out.corun_grid_index[o] = c;
@@ -367,7 +402,8 @@ struct ResolveArgs {
     const uint32_t *qcount;
 };
 
-__global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a) {
+__global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
+                                                 const __grid_constant__ Head64P net64) {
     const uint32_t count = *a.qcount;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -382,7 +418,7 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a) {
         int arg = INT_MAX;
         for (int c = lane; c < a.g.G; c += 32) {
             if (!((__ldg(a.g.mask + c) >> l) & 1u)) continue;
-            double tt = corun64(a.t, a.base_time, i, j, c);
+            double tt = corun64(a.t, net64, a.base_time, i, j, c);
             if (tt < best) { best = tt; arg = c; }          // ascending c per lane: first index
         }
         for (int off = 16; off; off >>= 1) {
@@ -483,10 +519,24 @@ int choose_log2_slices(int64_t P, int G) {
 }
 
 template <int L>
-void launch_sweep(const SweepArgs &a, const Net32P &net, cudaStream_t st) {
-    const int64_t threads = a.P << a.log2s;
-    const int64_t blocks = (threads + kSweepThreads - 1) / kSweepThreads;
-    k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net);
+int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int kind,
+                 cudaStream_t st) {
+    if (kind == CS_KERNEL_SIMT) {
+        const int64_t threads = a.P << a.log2s;
+        const int64_t blocks = (threads + kSweepThreads - 1) / kSweepThreads;
+        k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net, n64);
+        return CS_OK;
+    }
+    const size_t smem = tc_smem_bytes(a.g.G);
+    if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return CS_ERR_CUDA;
+    const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
+    int64_t ctas = (nblocks + tc::kGroups - 1) / tc::kGroups;
+    if (ctas > sm_count()) ctas = sm_count();
+    k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, n64);
+    return CS_OK;
 }
 
 }  // namespace
@@ -513,7 +563,7 @@ const char *cs_error_string(int code) {
 size_t cs_tables_bytes(int32_t n_apps, int32_t n_grid, int32_t n_solo) {
     if (n_apps < 0 || n_grid < 0 || n_solo < 0) return 0;
     size_t b = 0;
-    b += align256(sizeof(double) * NET64_LEN);
+    b += align256(sizeof(uint16_t) * W2_TILE_ELEMS);
     b += 2 * align256(sizeof(float) * (size_t)n_apps * ROW32);
     b += 2 * align256(sizeof(double) * (size_t)n_apps * HD);
     b += 2 * align256(sizeof(float) * (size_t)n_grid * ROW32);
@@ -529,7 +579,7 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
     char *p = (char *)d_base;
     auto take = [&p](size_t sz) { char *r = p; p += align256(sz); return (void *)r; };
     out->n_apps = n_apps; out->n_grid = n_grid; out->n_solo = n_solo;
-    out->net64 = (double *)take(sizeof(double) * NET64_LEN);
+    out->w2_tile = (uint16_t *)take(sizeof(uint16_t) * W2_TILE_ELEMS);
     out->app_a32 = (float *)take(sizeof(float) * (size_t)n_apps * ROW32);
     out->app_b32 = (float *)take(sizeof(float) * (size_t)n_apps * ROW32);
     out->app_a64 = (double *)take(sizeof(double) * (size_t)n_apps * HD);
@@ -551,21 +601,23 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
     GridP g = grid_params(d_grid);
     if (tables->n_apps != n_apps || tables->n_grid != g.G || tables->n_solo < g.S) return CS_ERR_ARG;
     const int64_t rows = (int64_t)n_apps + g.G + g.S;
-    int64_t threads = rows > NET64_LEN ? rows : NET64_LEN;
+    int64_t threads = rows > W2_TILE_ELEMS ? rows : W2_TILE_ELEMS;
     int blocks = (int)((threads + 127) / 128);
     k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables);
     return check_launch();
 }
 
-int cs_solo(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
-            cs_solo_out out, void *stream) {
+int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+            const double *d_base_time, cs_solo_out out, void *stream) {
+    Net64P n64;
+    if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
     if (rc) return rc;
     if (!tables || !d_base_time || !out.solo_time || !out.solo_split) return CS_ERR_ARG;
     GridP g = grid_params(d_grid);
-    const int64_t threads = (int64_t)tables->n_apps * g.L;
+    const int64_t threads = (int64_t)tables->n_apps * g.L * 32;
     k_solo<<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        *tables, g, d_base_time, tables->n_apps, out);
+        *tables, g, d_base_time, tables->n_apps, out, head64_from(n64));
     return check_launch();
 }
 
@@ -574,6 +626,16 @@ int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid 
                   const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
                   double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                   unsigned long long *d_clamps, void *stream) {
+    return cs_pair_sweep_ex(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
+                            pair_begin, pair_end, rel_eps, out, d_queue, d_queue_count, d_clamps,
+                            CS_KERNEL_AUTO, stream);
+}
+
+int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, int kernel_kind, void *stream) {
     Net64P n64;
     if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
@@ -608,24 +670,31 @@ int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid 
     a.qcount = d_queue_count;
     a.clamps = d_clamps;
     cudaStream_t st = (cudaStream_t)stream;
+    const Head64P h64 = head64_from(n64);
+    if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
+    if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT) return CS_ERR_ARG;
+    int lrc;
     switch (a.g.L) {
-        case 1: launch_sweep<1>(a, n32, st); break;
-        case 2: launch_sweep<2>(a, n32, st); break;
-        case 3: launch_sweep<3>(a, n32, st); break;
-        case 4: launch_sweep<4>(a, n32, st); break;
-        case 5: launch_sweep<5>(a, n32, st); break;
-        case 6: launch_sweep<6>(a, n32, st); break;
-        case 7: launch_sweep<7>(a, n32, st); break;
-        case 8: launch_sweep<8>(a, n32, st); break;
+        case 1: lrc = launch_sweep<1>(a, n32, h64, kernel_kind, st); break;
+        case 2: lrc = launch_sweep<2>(a, n32, h64, kernel_kind, st); break;
+        case 3: lrc = launch_sweep<3>(a, n32, h64, kernel_kind, st); break;
+        case 4: lrc = launch_sweep<4>(a, n32, h64, kernel_kind, st); break;
+        case 5: lrc = launch_sweep<5>(a, n32, h64, kernel_kind, st); break;
+        case 6: lrc = launch_sweep<6>(a, n32, h64, kernel_kind, st); break;
+        case 7: lrc = launch_sweep<7>(a, n32, h64, kernel_kind, st); break;
+        case 8: lrc = launch_sweep<8>(a, n32, h64, kernel_kind, st); break;
         default: return CS_ERR_ARG;
     }
+    if (lrc) return lrc;
     return check_launch();
 }
 
-int cs_resolve(const cs_tables *tables, const cs_grid *d_grid, const double *d_base_time,
-               const double *d_solo_time, int64_t pair_begin, int64_t pair_end,
-               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
-               void *stream) {
+int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+               const double *d_base_time, const double *d_solo_time, int64_t pair_begin,
+               int64_t pair_end, cs_pair_out out, const int64_t *d_queue,
+               const uint32_t *d_queue_count, void *stream) {
+    Net64P n64;
+    if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
     if (rc) return rc;
     if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count) return CS_ERR_ARG;
@@ -642,7 +711,7 @@ int cs_resolve(const cs_tables *tables, const cs_grid *d_grid, const double *d_b
     a.queue = d_queue;
     a.qcount = d_queue_count;
     // the queue length lives on the device: launch one resident wave, grid-stride
-    k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a);
+    k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a, head64_from(n64));
     return check_launch();
 }
 
@@ -751,13 +820,13 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     CS_RC(cs_build_tables(net, (const double *)(ws + L.feats), n_apps, &dg, &t, stream));
     cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
                    (int32_t *)(ws + L.solo_clamps)};
-    CS_RC(cs_solo(&t, &dg, (const double *)(ws + L.bt), so, stream));
+    CS_RC(cs_solo(net, &t, &dg, (const double *)(ws + L.bt), so, stream));
     cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
     CS_RC(cs_pair_sweep(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time, so.solo_clamps, 0, P,
                         rel_eps, po, (int64_t *)(ws + L.queue), (uint32_t *)(ws + L.qcount),
                         (unsigned long long *)(ws + L.clamps), stream));
-    CS_RC(cs_resolve(&t, &dg, (const double *)(ws + L.bt), so.solo_time, 0, P, po,
+    CS_RC(cs_resolve(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time, 0, P, po,
                      (const int64_t *)(ws + L.queue), (const uint32_t *)(ws + L.qcount), stream));
     for (int l = 0; l < nb && h_weights; ++l) {
         CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n, st));

@@ -106,7 +106,7 @@ class SweepPlan:
 
     def __init__(self, weights, grid: KnobGrid, n: int, pair_begin: int = 0,
                  pair_end: Optional[int] = None, device=None, with_matrix: bool = True,
-                 rel_eps: float = DEFAULT_REL_EPS):
+                 rel_eps: float = DEFAULT_REL_EPS, kernel: str = "tcgen05"):
         self.lib = nat.sweep_lib()
         self.device = require_cuda(device)
         if n < 2:
@@ -116,6 +116,10 @@ class SweepPlan:
         if not 0 <= pair_begin <= pair_end <= P_all:
             raise ValidationError(f"pair range [{pair_begin}, {pair_end}) outside [0, {P_all})")
         self.n, self.grid, self.rel_eps = n, grid, float(rel_eps)
+        kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT}
+        if kernel not in kinds:
+            raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
+        self.kernel, self.kernel_kind = kernel, kinds[kernel]
         self.pair_begin, self.pair_end = int(pair_begin), pair_end
         self.P = pair_end - pair_begin
         self.net = NetworkABI(weights)
@@ -175,21 +179,22 @@ class SweepPlan:
         tref = ctypes.byref(self.tables)
         nat.check(lib.cs_build_tables(self.net.ref(), _dptr(d_features), n, self.dgrid.ref(),
                                       tref, st), "cs_build_tables")
-        nat.check(lib.cs_solo(tref, self.dgrid.ref(), _dptr(d_base_time), self.solo_out, st),
-                  "cs_solo")
+        nat.check(lib.cs_solo(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
+                              self.solo_out, st), "cs_solo")
         if self.P == 0:
             return
         cnt = _dptr(self.counters)
         if sweep_events is not None:
             sweep_events[0].record()
-        nat.check(lib.cs_pair_sweep(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                                    _dptr(self.solo_time), _dptr(self.solo_clamps),
-                                    self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
-                                    _dptr(self.queue), cnt, _dptr(self.clamps), st),
-                  "cs_pair_sweep")
+        nat.check(lib.cs_pair_sweep_ex(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
+                                       _dptr(self.solo_time), _dptr(self.solo_clamps),
+                                       self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
+                                       _dptr(self.queue), cnt, _dptr(self.clamps),
+                                       self.kernel_kind, st), "cs_pair_sweep")
         if sweep_events is not None:
             sweep_events[1].record()
-        nat.check(lib.cs_resolve(tref, self.dgrid.ref(), _dptr(d_base_time), _dptr(self.solo_time),
+        nat.check(lib.cs_resolve(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
+                                 _dptr(self.solo_time),
                                  self.pair_begin, self.pair_end, self.pair_out, _dptr(self.queue),
                                  cnt, st), "cs_resolve")
         if self.matrix is not None:

@@ -38,16 +38,17 @@ def knob_grid(spaces: Sequence[ConfigSpace]) -> KnobGrid:
 
 def plan_for(weights, spaces: Sequence[ConfigSpace], n: int, pair_begin: int = 0,
              pair_end: Optional[int] = None, with_matrix: bool = True,
-             rel_eps: float = DEFAULT_REL_EPS) -> SweepPlan:
+             rel_eps: float = DEFAULT_REL_EPS, kernel: str = "tcgen05") -> SweepPlan:
     """A cached SweepPlan (buffers are reused across calls of the same shape)."""
     dev = require_cuda()
-    key = (id(weights), tuple(spaces), n, pair_begin, pair_end, with_matrix, rel_eps, str(dev))
+    key = (id(weights), tuple(spaces), n, pair_begin, pair_end, with_matrix, rel_eps, kernel,
+           str(dev))
     hit = _PLAN_CACHE.get(key)
     if hit is not None and hit[0] is weights:
         _PLAN_CACHE.move_to_end(key)
         return hit[1]
     plan = SweepPlan(weights, knob_grid(spaces), n, pair_begin, pair_end, dev,
-                     with_matrix=with_matrix, rel_eps=rel_eps)
+                     with_matrix=with_matrix, rel_eps=rel_eps, kernel=kernel)
     _PLAN_CACHE[key] = (weights, plan)          # holds `weights` so its id stays unique
     while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
         _PLAN_CACHE.popitem(last=False)
@@ -116,7 +117,8 @@ def run_plan(plan: SweepPlan, features: np.ndarray, base_time: np.ndarray,
 
 def sweep_pairs(weights, jobs: Sequence[JobProfile], spaces, pair_begin: int = 0,
                 pair_end: Optional[int] = None, with_matrix: bool = True,
-                need_corun: bool = True, need_solo: bool = True) -> SweepResult:
+                need_corun: bool = True, need_solo: bool = True,
+                kernel: str = "tcgen05") -> SweepResult:
     """Evaluate every (pair, config) of `jobs` for each budget in `spaces` on the GPU.
 
     Raises the reference's ValidationErrors for an empty co-run space
@@ -129,5 +131,6 @@ def sweep_pairs(weights, jobs: Sequence[JobProfile], spaces, pair_begin: int = 0
         raise ValidationError("a sweep needs at least two jobs")
     knob_grid(tuple(spaces)).check_nonempty(corun=need_corun, solo=need_solo)
     feats, bt = _inputs(jobs)
-    plan = plan_for(weights, tuple(spaces), len(jobs), pair_begin, pair_end, with_matrix)
+    plan = plan_for(weights, tuple(spaces), len(jobs), pair_begin, pair_end, with_matrix,
+                    kernel=kernel)
     return run_plan(plan, feats, bt, with_matrix)

@@ -1,0 +1,50 @@
+"""The tcgen05 screen (k_sweep_tc) and the SIMT screen agree with the oracle bit-for-bit."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import workload
+from paper_2405_03831_b200 import core, synth
+from paper_2405_03831_b200.grid import KnobGrid
+from paper_2405_03831_b200.sweep import sweep_pairs
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(res, ref, L):
+    for l in range(L):
+        assert np.array_equal(res.corun_grid_index[l], ref["corun_grid_index"][l])
+        assert np.array_equal(res.corun_chosen[l], ref["corun_chosen"][l])
+        assert np.array_equal(res.corun_time[l], ref["corun_time"][l])
+        assert np.array_equal(res.weight[l], ref["weight"][l])
+
+
+@pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
+@pytest.mark.parametrize("n,seed,budgets", [
+    (20, 0, (400.0,)), (2, 1, (400.0,)), (67, 2, (350.0,)), (131, 3, (400.0, 350.0)),
+    (256, 0, (400.0,))])
+def test_screen_kernels_match_oracle(weights, kernel, n, seed, budgets):
+    spaces = [core.default_space(p) for p in budgets]
+    jobs = synth.generate_workload(seed, synth.mixed_archetypes(n))
+    res = sweep_pairs(weights, jobs, spaces, with_matrix=False, kernel=kernel)
+    F, T = workload(n, seed)
+    ref = oracle.sweep(weights, F, T, KnobGrid(spaces))
+    _check(res, ref, len(spaces))
+    assert res.screen_error < 1e-5, res.screen_error
+
+
+@pytest.mark.parametrize("kernel", ["tcgen05", "simt"])
+def test_five_budgets_and_fine_grid_shards(weights, kernel):
+    levels = (300, 325, 350, 375, 400)
+    spaces = [core.ConfigSpace(p_total=p, cap_sum_levels=levels) for p in (300.0, 325.0, 350.0, 375.0, 400.0)]
+    n = 1024
+    jobs = synth.generate_workload(0, synth.mixed_archetypes(n))
+    F, T = workload(n)
+    b, e = 123_456, 123_456 + 5000
+    res = sweep_pairs(weights, jobs, spaces, b, e, with_matrix=False, kernel=kernel)
+    _check(res, oracle.sweep(weights, F, T, KnobGrid(spaces), b, e), 5)
+    fine = [core.ConfigSpace(cpu_caps=tuple(100.0 + 6.25 * k for k in range(25)),
+                             gpu_caps=tuple(150.0 + 6.25 * k for k in range(17)), p_total=400.0)]
+    res = sweep_pairs(weights, jobs, fine, b, e, with_matrix=False, kernel=kernel)
+    _check(res, oracle.sweep(weights, F, T, KnobGrid(fine), b, e), 1)
