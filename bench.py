@@ -246,7 +246,7 @@ def run_ours(args):
     ev_s = torch.cuda.Event(enable_timing=True, external=True)
     ev_e = torch.cuda.Event(enable_timing=True, external=True)
     if world == 1:
-        plan = SweepPlan(weights, grid, n, device=dev, with_matrix=True)
+        plan = SweepPlan(weights, grid, n, device=dev, with_matrix=True, kernel=args.kernel)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -262,7 +262,7 @@ def run_ours(args):
         units_local = P * upp
     else:
         from paper_2405_03831_b200.dist import ShardedSweep
-        sh = ShardedSweep(weights, grid, n, device=dev)
+        sh = ShardedSweep(weights, grid, n, device=dev, kernel=args.kernel)
         plan = sh.plan
 
         def step():
@@ -321,7 +321,8 @@ def run_ours(args):
                        "parallelism": f"pair shards x{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tf,
                          "unit": "TFLOP/s", "frac": achieved_tflops / tf, "traffic": None,
-                         "kernel": "k_sweep", "kernel_ms": sweep_avg,
+                         "kernel": "k_sweep_tc (tcgen05)" if args.kernel == "tcgen05" else
+                                   "k_sweep (SIMT fp32)", "kernel_ms": sweep_avg,
                          "flops_per_unit": FLOPS_PER_UNIT, "units_per_launch": units_local,
                          "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
                          "kernel_share_of_step": sweep_avg / (total_ms / args.steps)},
@@ -386,6 +387,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--workload", default="n256", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "simt"],
+                    help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 namespace {
 
@@ -177,6 +178,7 @@ struct SweepArgs {
     int64_t *queue;
     uint32_t *qcount;
     unsigned long long *clamps;
+    uint32_t *trace;         // debug builds (CS_TC_TRACE): per-thread progress, host-mapped
 };
 
 __device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
@@ -477,6 +479,13 @@ __global__ void k_forward_rows(const __grid_constant__ Net64P net, const double 
     }
 }
 
+#ifdef CS_TC_TRACE
+void *getenv_ptr(const char *name) {
+    const char *v = getenv(name);
+    return v ? (void *)strtoull(v, nullptr, 0) : nullptr;
+}
+#endif
+
 int sm_count() {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess)
@@ -669,6 +678,10 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
     a.queue = d_queue;
     a.qcount = d_queue_count;
     a.clamps = d_clamps;
+    a.trace = nullptr;
+#ifdef CS_TC_TRACE
+    a.trace = (uint32_t *)getenv_ptr("CS_TC_TRACE_PTR");
+#endif
     cudaStream_t st = (cudaStream_t)stream;
     const Head64P h64 = head64_from(n64);
     if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;

@@ -26,6 +26,14 @@
 // shared with the SIMT kernel, so results are identical.
 #pragma once
 
+#ifdef CS_TC_TRACE
+#define TC_TRACE(stage, k) \
+    do { if (a.trace) ((volatile uint32_t *)a.trace)[blockIdx.x * tc::kThreads + threadIdx.x] = \
+             ((uint32_t)(k) << 8) | (stage); } while (0)
+#else
+#define TC_TRACE(stage, k) do { } while (0)
+#endif
+
 namespace tc {
 
 constexpr int kGroups = 4;
@@ -216,7 +224,9 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
         for (int i = 0; i < 2 * tc::kGroups; ++i) tc::mbar_init(&mbars[i], 1);
         tc::fence_mbar_init();
     }
+    TC_TRACE(1, 0);
     if (warp == 0) tc::tmem_alloc(tmem_slot, tc::kGroups * tc::kTmemColsPerGroup);
+    TC_TRACE(2, 0);
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
@@ -287,7 +297,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
             }
             tc::fence_proxy_async();
             tc::fence_before();
+            __syncwarp();
+            TC_TRACE(3, k);
             tc::group_bar(g);
+            TC_TRACE(4, k);
             // ---- 2. one thread issues the MMAs of config k ----
             if (k < a.g.G && t == 0) {
                 tc::fence_after();
@@ -299,10 +312,14 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                                 tc::smem_desc(b_addr + s * 256), s > 0);
                 tc::mma_commit(&mbars[2 * g + (k & 1)]);
             }
+            __syncwarp();
+            TC_TRACE(5, k);
             // ---- 3. epilogue of config k-1 ----
             if (k >= 1) {
                 const int c = k - 1, b = c & 1;
                 tc::mbar_wait(&mbars[2 * g + b], phase[b]);
+                __syncwarp();
+                TC_TRACE(6, k);
                 phase[b] ^= 1u;
                 tc::fence_after();
                 float z[HD];
@@ -331,6 +348,11 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                 atomicAdd(a.clamps + l, (unsigned long long)(a.solo_clamps[(size_t)l * a.n + i] +
                                                              a.solo_clamps[(size_t)l * a.n + j]));
             const bool ambiguous = !(second[l] > best[l] * (1.0f + a.eps));
+            const int c = idx[l];
+            // every lane reaches the shuffle (ambiguity differs across the warp's pairs)
+            const double tm64 =
+                ambiguous ? 0.0 : member_time64(a.t, net64, a.base_time, self, other, c, member);
+            const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
             if (ambiguous) {
                 if (live && member == 0) {
                     const uint32_t q = atomicAdd(a.qcount, 1u);
@@ -338,9 +360,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                 }
                 continue;
             }
-            const int c = idx[l];
-            const double tm64 = member_time64(a.t, net64, a.base_time, self, other, c, member);
-            const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
             if (live && member == 0) {
                 const int64_t o = (int64_t)l * a.P + pl;
                 const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) +
@@ -355,6 +374,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
             }
         }
     }
+    TC_TRACE(7, 0);
     // clamp counters: one atomic per warp and budget
 #pragma unroll
     for (int l = 0; l < L; ++l) {
@@ -367,6 +387,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
         tc::fence_after();
         tc::tmem_dealloc(tmem_base, tc::kGroups * tc::kTmemColsPerGroup);
     }
+    TC_TRACE(8, 0);
 }
 
 inline size_t tc_smem_bytes(int G) {

@@ -62,7 +62,8 @@ def gather_records(local: dict, P: int, group: Optional[dist.ProcessGroup] = Non
 class ShardedSweep:
     """A SweepPlan on this rank's pair shard plus the gather and the device scatter."""
 
-    def __init__(self, weights, grid, n: int, group=None, device=None, rel_eps=None):
+    def __init__(self, weights, grid, n: int, group=None, device=None, rel_eps=None,
+                 kernel: str = "tcgen05"):
         from .device import DEFAULT_REL_EPS, SweepPlan
         self.group = group
         self.rank = dist.get_rank(group)
@@ -71,7 +72,8 @@ class ShardedSweep:
         self.P = n * (n - 1) // 2
         b, e = shard_range(self.P, self.rank, self.world)
         self.plan = SweepPlan(weights, grid, n, b, e, device=device, with_matrix=False,
-                              rel_eps=DEFAULT_REL_EPS if rel_eps is None else rel_eps)
+                              rel_eps=DEFAULT_REL_EPS if rel_eps is None else rel_eps,
+                              kernel=kernel)
         self.matrix = torch.zeros((grid.n_budgets, n, n), dtype=torch.float64,
                                   device=self.plan.device)
 
