@@ -63,9 +63,11 @@ enum {
 /* Screen kernels of cs_pair_sweep_ex (results are identical: both feed the same
  * exact fp64 re-evaluation / re-scan). */
 enum {
-    CS_KERNEL_AUTO = 0,       /* tcgen05 on sm_100a                                       */
-    CS_KERNEL_TCGEN05 = 1,    /* layer 2 on the tensor cores: fp16 3-term split, fp32 acc */
-    CS_KERNEL_SIMT = 2        /* layer 2 as fp32 FFMA with W2 in the parameter bank       */
+    CS_KERNEL_AUTO = 0,          /* tcgen05 on sm_100a                                    */
+    CS_KERNEL_TCGEN05 = 1,       /* layer 2 on tensor cores, A operand in TMEM, fp16 3-term
+                                    split, fp32 accumulate                                */
+    CS_KERNEL_SIMT = 2,          /* layer 2 as fp32 FFMA with W2 in the parameter bank    */
+    CS_KERNEL_TCGEN05_SMEM_A = 3 /* tensor cores with the A operand staged in SMEM (v2)   */
 };
 
 /* NetworkWeights (fnn.py:42-68), HOST fp64, row-major exactly as the

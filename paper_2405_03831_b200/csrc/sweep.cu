@@ -34,7 +34,7 @@ constexpr int NF = CS_NUM_FEATURES;
 constexpr int HD = CS_HIDDEN;
 constexpr int IN = CS_INPUT_DIM;
 constexpr int ROW32 = 20;                  // fp32 table row: 18 + 2 pad (80 B, float4-aligned)
-constexpr int W2_TILE_ELEMS = 32 * 64;     // fp16 B tile of the tcgen05 screen
+constexpr int W2_TILE_ELEMS = 2 * 32 * 64; // fp16 B operands: v2 tile | v3 slices
 constexpr double FLOOR = 0.5;              // estimator.py:33
 constexpr int kSweepThreads = 128;
 
@@ -207,6 +207,7 @@ __device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&
 }
 
 #include "tc_sweep.cuh"
+#include "tc2_sweep.cuh"
 
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -214,7 +215,8 @@ __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v >
 __global__ void k_tables(const __grid_constant__ Net64P net, const double *__restrict__ feats,
                          int n, const GridP g, const cs_tables t) {
     int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid < W2_TILE_ELEMS) write_b_tile(net, t.w2_tile, (int)tid);
+    if (tid < W2_TILE_ELEMS / 2) write_b_tile(net, t.w2_tile, (int)tid);
+    else if (tid < W2_TILE_ELEMS) write_b_slices(net, t.w2_tile + W2_TILE_ELEMS / 2, (int)tid - W2_TILE_ELEMS / 2);
     const int64_t rows = (int64_t)n + g.G + g.S;
     for (int64_t r = tid; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
         if (r < n) {
@@ -536,15 +538,24 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int 
         k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net, n64);
         return CS_OK;
     }
-    const size_t smem = tc_smem_bytes(a.g.G);
-    if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
-    cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return CS_ERR_CUDA;
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
     int64_t ctas = (nblocks + tc::kGroups - 1) / tc::kGroups;
     if (ctas > sm_count()) ctas = sm_count();
-    k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, n64);
+    if (kind == CS_KERNEL_TCGEN05_SMEM_A) {
+        const size_t smem = tc_smem_bytes(a.g.G);
+        if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
+        if (cudaFuncSetAttribute(k_sweep_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return CS_ERR_CUDA;
+        k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, n64);
+        return CS_OK;
+    }
+    const size_t smem = tc2_smem_bytes(a.g.G);
+    if (smem > 227 * 1024) return CS_ERR_ARG;
+    if (cudaFuncSetAttribute(k_sweep_tc2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return CS_ERR_CUDA;
+    k_sweep_tc2<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, n64);
     return CS_OK;
 }
 
@@ -685,7 +696,9 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
     cudaStream_t st = (cudaStream_t)stream;
     const Head64P h64 = head64_from(n64);
     if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
-    if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT) return CS_ERR_ARG;
+    if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
+        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A)
+        return CS_ERR_ARG;
     int lrc;
     switch (a.g.L) {
         case 1: lrc = launch_sweep<1>(a, n32, h64, kernel_kind, st); break;

@@ -116,7 +116,8 @@ class SweepPlan:
         if not 0 <= pair_begin <= pair_end <= P_all:
             raise ValidationError(f"pair range [{pair_begin}, {pair_end}) outside [0, {P_all})")
         self.n, self.grid, self.rel_eps = n, grid, float(rel_eps)
-        kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT}
+        kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT,
+                 "tcgen05_smem": nat.KERNEL_TCGEN05_SMEM_A}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
