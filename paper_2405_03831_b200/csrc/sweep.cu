@@ -555,7 +555,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int 
     if (cudaFuncSetAttribute(k_sweep_tc2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return CS_ERR_CUDA;
-    k_sweep_tc2<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, n64);
+    k_sweep_tc2<L><<<(unsigned)ctas, kTc2Threads, smem, st>>>(a, net, n64);
     return CS_OK;
 }
 

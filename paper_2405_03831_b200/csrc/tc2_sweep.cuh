@@ -72,6 +72,10 @@ __device__ __forceinline__ void tmem_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {
     unsigned long long r, x = *reinterpret_cast<unsigned long long *>(&a),
                           y = *reinterpret_cast<unsigned long long *>(&b);
@@ -114,8 +118,10 @@ __device__ void write_b_slices(const Net64P &net, uint16_t *tile, int idx) {
     tile[off / 2] = *reinterpret_cast<uint16_t *>(&h);
 }
 
+constexpr int kTc2Threads = tc::kThreads + 32;   // 4 groups x 128 + 1 MMA-issuer warp
+
 template <int L>
-__global__ void __launch_bounds__(tc::kThreads, 1)
+__global__ void __launch_bounds__(kTc2Threads, 1)
     k_sweep_tc2(const SweepArgs a, const __grid_constant__ Net32P net,
                 const __grid_constant__ Head64P net64) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -124,25 +130,32 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     float *k1s = reinterpret_cast<float *>(smem + tc2::kBBytes);
     float *k2s = k1s + (size_t)a.g.G * ROW32;
     uint32_t *masks = reinterpret_cast<uint32_t *>(k2s + (size_t)a.g.G * ROW32);
+    // d_ready[g][b]: MMA -> epilogue (tcgen05.commit, count 1)
+    // a_ready[g][b]: A rows in TMEM -> MMA issuer (one arrive per compute warp, count 4)
     uint64_t *mbars = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbars + 2 * tc::kGroups);
+    uint64_t *a_ready = mbars + 2 * tc::kGroups;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + 2 * tc::kGroups);
 
     const int tid = threadIdx.x;
-    const int g = tid / tc::kGroupThreads;
+    const int g = tid / tc::kGroupThreads;     // 4 = the MMA-issuer warp
     const int t = tid % tc::kGroupThreads;
     const int warp = tid >> 5;
+    const int lane = tid & 31;
 
-    for (int i = tid; i < tc2::kBBytes / 16; i += tc::kThreads)
+    for (int i = tid; i < tc2::kBBytes / 16; i += kTc2Threads)
         reinterpret_cast<uint4 *>(b_tile)[i] =
             reinterpret_cast<const uint4 *>(a.t.w2_tile + tc::kBBytes / 2)[i];
-    for (int i = tid; i < a.g.G * ROW32; i += tc::kThreads) {
+    for (int i = tid; i < a.g.G * ROW32; i += kTc2Threads) {
         k1s[i] = a.t.knob1_32[i];
         k2s[i] = a.t.knob2_32[i];
     }
-    for (int i = tid; i < a.g.G; i += tc::kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
+    for (int i = tid; i < a.g.G; i += kTc2Threads) masks[i] = L == 1 ? 1u : a.g.mask[i];
     if (tid == 0) {
-        for (int i = 0; i < 2 * tc::kGroups; ++i) tc::mbar_init(&mbars[i], 1);
+        for (int i = 0; i < 2 * tc::kGroups; ++i) {
+            tc::mbar_init(&mbars[i], 1);
+            tc::mbar_init(&a_ready[i], 4);
+        }
         tc::fence_mbar_init();
     }
     if (warp == 0) tc::tmem_alloc(tmem_slot, tc::kGroups * tc2::kColsPerGroup);
@@ -151,6 +164,48 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
+    const int64_t total_groups = (int64_t)gridDim.x * tc::kGroups;
+
+    if (g == tc::kGroups) {
+        // ===== MMA issuer warp: serves the 4 groups as their A tiles land =====
+        const uint32_t b_addr = tc::smem_u32(b_tile);
+        const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
+                       bq2 = tc2::slice_desc(b_addr + 2048), bq3 = tc2::slice_desc(b_addr + 3072);
+        int64_t blk[tc::kGroups];
+        int kk[tc::kGroups];
+        uint32_t aph = 0;                              // bit (2g + b): parity of a_ready[g][b]
+#pragma unroll
+        for (int q = 0; q < tc::kGroups; ++q) { blk[q] = (int64_t)blockIdx.x * tc::kGroups + q; kk[q] = 0; }
+        long long t0 = clock64();
+        for (;;) {
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < tc::kGroups; ++q) {
+                if (blk[q] >= nblocks) continue;
+                any = true;
+                const int b = kk[q] & 1;
+                if (!tc::mbar_try(&a_ready[2 * q + b], (aph >> (2 * q + b)) & 1u)) continue;
+                aph ^= 1u << (2 * q + b);
+                t0 = clock64();
+                tc::fence_after();
+                if (lane == 0) {
+                    const uint32_t gc = tmem_base + q * tc2::kColsPerGroup;
+                    const uint32_t a_t = gc + b * 32, d_t = gc + 64 + b * 32;
+                    tc2::mma_ts(d_t, a_t + 0, bq0, 0);
+                    tc2::mma_ts(d_t, a_t + 8, bq0, 1);
+                    tc2::mma_ts(d_t, a_t + 16, bq1, 1);
+                    tc2::mma_ts(d_t, a_t + 0, bq2, 1);
+                    tc2::mma_ts(d_t, a_t + 16, bq3, 1);
+                    tc::mma_commit(&mbars[2 * q + b]);
+                }
+                __syncwarp();
+                if (++kk[q] == a.g.G) { kk[q] = 0; blk[q] += total_groups; }
+            }
+            if (!any) break;
+            if (clock64() - t0 > 4000000000LL) __trap();   // no progress for ~2 s: fail, don't hang
+        }
+    } else {
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t gcol = tmem_base + g * tc2::kColsPerGroup;   // + lane bits where needed
     // zero the never-written tail (columns 20-23) of both A buffers of this lane
@@ -165,10 +220,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     int clamps[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) clamps[l] = 0;
-    const uint32_t b_addr = tc::smem_u32(b_tile);
-
-    const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
-    const int64_t total_groups = (int64_t)gridDim.x * tc::kGroups;
     const int member = t & 1;
 
     for (int64_t blk = (int64_t)blockIdx.x * tc::kGroups + g; blk < nblocks; blk += total_groups) {
@@ -221,23 +272,12 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                 w[19] = 0u;
                 tc2::tmem_st20(gcol + lane_off + (k & 1) * 32, w);
                 tc2::tmem_st_wait();
+                // order this warp's TMEM stores (and its earlier TMEM loads of the
+                // same D buffer) before the issuer's MMA, then signal A(k) ready
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc2::mbar_arrive(&a_ready[2 * g + (k & 1)]);
             }
-            tc::fence_before();
-            __syncwarp();
-            tc::group_bar(g);
-            // ---- 2. one thread issues the 5 MMAs of config k ----
-            if (k < a.g.G && t == 0) {
-                tc::fence_after();
-                const uint32_t a_t = gcol + (k & 1) * 32;        // lane 0, A buffer
-                const uint32_t d_t = gcol + 64 + (k & 1) * 32;   // lane 0, D buffer
-                tc2::mma_ts(d_t, a_t + 0, tc2::slice_desc(b_addr + 0 * tc2::kBSliceBytes), 0);
-                tc2::mma_ts(d_t, a_t + 8, tc2::slice_desc(b_addr + 0 * tc2::kBSliceBytes), 1);
-                tc2::mma_ts(d_t, a_t + 16, tc2::slice_desc(b_addr + 1 * tc2::kBSliceBytes), 1);
-                tc2::mma_ts(d_t, a_t + 0, tc2::slice_desc(b_addr + 2 * tc2::kBSliceBytes), 1);
-                tc2::mma_ts(d_t, a_t + 16, tc2::slice_desc(b_addr + 3 * tc2::kBSliceBytes), 1);
-                tc::mma_commit(&mbars[2 * g + (k & 1)]);
-            }
-            __syncwarp();
             // ---- 3. epilogue of config k-1 ----
             if (k >= 1) {
                 const int c = k - 1, b = c & 1;
@@ -302,8 +342,9 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
 #pragma unroll
     for (int l = 0; l < L; ++l) {
         const int tot = __reduce_add_sync(0xffffffffu, clamps[l]);
-        if ((tid & 31) == 0 && tot) atomicAdd(a.clamps + l, (unsigned long long)tot);
+        if (lane == 0 && tot) atomicAdd(a.clamps + l, (unsigned long long)tot);
     }
+    }   // compute groups
     tc::fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -316,6 +357,6 @@ inline size_t tc2_smem_bytes(int G) {
     size_t b = (size_t)tc2::kBBytes;
     b += 2 * (size_t)G * ROW32 * sizeof(float) + (size_t)G * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * tc::kGroups * sizeof(uint64_t) + 16;
+    b += 4 * tc::kGroups * sizeof(uint64_t) + 16;
     return b;
 }
