@@ -118,7 +118,7 @@ __device__ void write_b_slices(const Net64P &net, uint16_t *tile, int idx) {
     tile[off / 2] = *reinterpret_cast<uint16_t *>(&h);
 }
 
-constexpr int kTc2Threads = tc::kThreads + 32;   // 4 groups x 128 + 1 MMA-issuer warp
+constexpr int kTc2Threads = tc::kThreads + 32 * tc::kGroups;   // 4 groups x 128 + 4 MMA-issuer warps
 
 template <int L>
 __global__ void __launch_bounds__(kTc2Threads, 1)
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + 2 * tc::kGroups);
 
     const int tid = threadIdx.x;
-    const int g = tid / tc::kGroupThreads;     // 4 = the MMA-issuer warp
+    const int g = tid / tc::kGroupThreads;     // 4 = the MMA-issuer warps
     const int t = tid % tc::kGroupThreads;
     const int warp = tid >> 5;
     const int lane = tid & 31;
@@ -167,30 +167,22 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
     const int64_t total_groups = (int64_t)gridDim.x * tc::kGroups;
 
-    if (g == tc::kGroups) {
-        // ===== MMA issuer warp: serves the 4 groups as their A tiles land =====
+    if (g >= tc::kGroups) {
+        // ===== MMA issuer warps: warp 16 + q serves group q =====
+        const int q = warp - tc::kGroups * (tc::kGroupThreads / 32);
         const uint32_t b_addr = tc::smem_u32(b_tile);
         const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
                        bq2 = tc2::slice_desc(b_addr + 2048), bq3 = tc2::slice_desc(b_addr + 3072);
-        int64_t blk[tc::kGroups];
-        int kk[tc::kGroups];
-        uint32_t aph = 0;                              // bit (2g + b): parity of a_ready[g][b]
-#pragma unroll
-        for (int q = 0; q < tc::kGroups; ++q) { blk[q] = (int64_t)blockIdx.x * tc::kGroups + q; kk[q] = 0; }
-        long long t0 = clock64();
-        for (;;) {
-            bool any = false;
-#pragma unroll
-            for (int q = 0; q < tc::kGroups; ++q) {
-                if (blk[q] >= nblocks) continue;
-                any = true;
-                const int b = kk[q] & 1;
-                if (!tc::mbar_try(&a_ready[2 * q + b], (aph >> (2 * q + b)) & 1u)) continue;
-                aph ^= 1u << (2 * q + b);
-                t0 = clock64();
+        const uint32_t gc = tmem_base + q * tc2::kColsPerGroup;
+        uint32_t aph = 0;                              // bit b: parity of a_ready[q][b]
+        for (int64_t blk = (int64_t)blockIdx.x * tc::kGroups + q; blk < nblocks; blk += total_groups) {
+            for (int k = 0; k < a.g.G; ++k) {
+                const int b = k & 1;
+                tc::mbar_wait(&a_ready[2 * q + b], (aph >> b) & 1u);
+                aph ^= 1u << b;
+                __syncwarp();
                 tc::fence_after();
                 if (lane == 0) {
-                    const uint32_t gc = tmem_base + q * tc2::kColsPerGroup;
                     const uint32_t a_t = gc + b * 32, d_t = gc + 64 + b * 32;
                     tc2::mma_ts(d_t, a_t + 0, bq0, 0);
                     tc2::mma_ts(d_t, a_t + 8, bq0, 1);
@@ -200,10 +192,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
                     tc::mma_commit(&mbars[2 * q + b]);
                 }
                 __syncwarp();
-                if (++kk[q] == a.g.G) { kk[q] = 0; blk[q] += total_groups; }
             }
-            if (!any) break;
-            if (clock64() - t0 > 4000000000LL) __trap();   // no progress for ~2 s: fail, don't hang
         }
     } else {
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -216,7 +205,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
     float2 wo2[9];
 #pragma unroll
     for (int o = 0; o < 9; ++o) wo2[o] = make_float2(net.wo[2 * o], net.wo[2 * o + 1]);
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phase = 0;                        // bit b: parity of d_ready[g][b]
     int clamps[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) clamps[l] = 0;
@@ -281,9 +270,9 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
             // ---- 3. epilogue of config k-1 ----
             if (k >= 1) {
                 const int c = k - 1, b = c & 1;
-                tc::mbar_wait(&mbars[2 * g + b], phase[b]);
+                tc::mbar_wait(&mbars[2 * g + b], (phase >> b) & 1u);
                 __syncwarp();
-                phase[b] ^= 1u;
+                phase ^= 1u << b;
                 tc::fence_after();
                 float z[HD];
                 tc::tmem_ld18(gcol + lane_off + 64 + b * 32, z);
