@@ -387,7 +387,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--workload", default="n256", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "tcgen05_smem", "simt"],
+    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "tcgen05_smem", "simt", "tcgen05_g4s2", "tcgen05_g3s3",
+                             "tcgen05_g2s4"],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -552,11 +552,23 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int 
     }
     const size_t smem = tc2_smem_bytes(a.g.G);
     if (smem > 227 * 1024) return CS_ERR_ARG;
-    if (cudaFuncSetAttribute(k_sweep_tc2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return CS_ERR_CUDA;
-    k_sweep_tc2<L><<<(unsigned)ctas, kTc2Threads, smem, st>>>(a, net, n64);
-    return CS_OK;
+    // (compute groups, pipeline stages) of the TMEM-A screen; CS_KERNEL_TCGEN05
+    // uses the measured best, 0x1GS kinds select a variant for tuning
+    int G = 3, S = 3;
+    if ((kind & 0xF00) == 0x100) { G = (kind >> 4) & 0xF; S = kind & 0xF; }
+    auto go = [&](auto kern, int groups, int threads) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return CS_ERR_CUDA;
+        int64_t c = (nblocks + groups - 1) / groups;
+        if (c > sm_count()) c = sm_count();
+        kern<<<(unsigned)c, threads, smem, st>>>(a, net, n64);
+        return CS_OK;
+    };
+    if (G == 4 && S == 2) return go(k_sweep_tc2<L, 4, 2>, 4, Tc2Cfg<4, 2>::kThreads);
+    if (G == 3 && S == 3) return go(k_sweep_tc2<L, 3, 3>, 3, Tc2Cfg<3, 3>::kThreads);
+    if (G == 2 && S == 4) return go(k_sweep_tc2<L, 2, 4>, 2, Tc2Cfg<2, 4>::kThreads);
+    return CS_ERR_ARG;
 }
 
 }  // namespace
@@ -697,7 +709,7 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
     const Head64P h64 = head64_from(n64);
     if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
     if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
-        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A)
+        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100)
         return CS_ERR_ARG;
     int lrc;
     switch (a.g.L) {

@@ -26,7 +26,6 @@ namespace tc2 {
 
 constexpr int kBSliceBytes = 32 * 16 * 2;     // N=32 rows x 16 halves
 constexpr int kBBytes = 4 * kBSliceBytes;     // 4 KB
-constexpr int kColsPerGroup = 128;            // A0 | A1 | D0 | D1, 32 columns each
 
 // canonical no-swizzle K-major slice: 8x16 B core matrices, LBO 128 B, SBO 256 B
 __host__ __device__ __forceinline__ uint32_t slice_off(int row, int chunk) {
@@ -118,100 +117,113 @@ __device__ void write_b_slices(const Net64P &net, uint16_t *tile, int idx) {
     tile[off / 2] = *reinterpret_cast<uint16_t *>(&h);
 }
 
-constexpr int kTc2Threads = tc::kThreads + 32 * tc::kGroups;   // 4 groups x 128 + 4 MMA-issuer warps
+// TMEM map (columns): all D stages first (32 columns each, 32-aligned), then all
+// A stages (24 columns each): D(g, s) = (g*S + s)*32, A(g, s) = G*S*32 + (g*S + s)*24.
+template <int G, int S>
+struct Tc2Cfg {
+    static constexpr int kThreads = G * tc::kGroupThreads + G * 32;   // + one issuer warp per group
+    static constexpr int kCols = G * S * 56;
+    static_assert(kCols <= 512, "TMEM holds 512 columns");
+    __device__ static constexpr uint32_t d_col(int g, int s) { return (uint32_t)((g * S + s) * 32); }
+    __device__ static constexpr uint32_t a_col(int g, int s) {
+        return (uint32_t)(G * S * 32 + (g * S + s) * 24);
+    }
+};
 
-template <int L>
-__global__ void __launch_bounds__(kTc2Threads, 1)
+template <int L, int G, int S>
+__global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
     k_sweep_tc2(const SweepArgs a, const __grid_constant__ Net32P net,
                 const __grid_constant__ Head64P net64) {
+    using Cfg = Tc2Cfg<G, S>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    // carve: [B slices 4 KB][K1 | K2 fp32 G x 20][mask G][mbar 8][tmem slot]
+    // carve: [B slices 4 KB][K1 | K2 fp32 G x 20][mask G][d_ready G*S][a_ready G*S][tmem slot]
     uint8_t *b_tile = smem;
     float *k1s = reinterpret_cast<float *>(smem + tc2::kBBytes);
     float *k2s = k1s + (size_t)a.g.G * ROW32;
     uint32_t *masks = reinterpret_cast<uint32_t *>(k2s + (size_t)a.g.G * ROW32);
-    // d_ready[g][b]: MMA -> epilogue (tcgen05.commit, count 1)
-    // a_ready[g][b]: A rows in TMEM -> MMA issuer (one arrive per compute warp, count 4)
-    uint64_t *mbars = reinterpret_cast<uint64_t *>(
+    // d_ready[g*S+s]: MMA -> epilogue (tcgen05.commit, count 1)
+    // a_ready[g*S+s]: A rows in TMEM -> MMA issuer (one arrive per compute warp, count 4)
+    uint64_t *d_ready = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
-    uint64_t *a_ready = mbars + 2 * tc::kGroups;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + 2 * tc::kGroups);
+    uint64_t *a_ready = d_ready + G * S;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + G * S);
 
     const int tid = threadIdx.x;
-    const int g = tid / tc::kGroupThreads;     // 4 = the MMA-issuer warps
+    const int g = tid / tc::kGroupThreads;     // >= G: the MMA-issuer warps
     const int t = tid % tc::kGroupThreads;
     const int warp = tid >> 5;
     const int lane = tid & 31;
 
-    for (int i = tid; i < tc2::kBBytes / 16; i += kTc2Threads)
+    for (int i = tid; i < tc2::kBBytes / 16; i += Cfg::kThreads)
         reinterpret_cast<uint4 *>(b_tile)[i] =
             reinterpret_cast<const uint4 *>(a.t.w2_tile + tc::kBBytes / 2)[i];
-    for (int i = tid; i < a.g.G * ROW32; i += kTc2Threads) {
+    for (int i = tid; i < a.g.G * ROW32; i += Cfg::kThreads) {
         k1s[i] = a.t.knob1_32[i];
         k2s[i] = a.t.knob2_32[i];
     }
-    for (int i = tid; i < a.g.G; i += kTc2Threads) masks[i] = L == 1 ? 1u : a.g.mask[i];
+    for (int i = tid; i < a.g.G; i += Cfg::kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
     if (tid == 0) {
-        for (int i = 0; i < 2 * tc::kGroups; ++i) {
-            tc::mbar_init(&mbars[i], 1);
+        for (int i = 0; i < G * S; ++i) {
+            tc::mbar_init(&d_ready[i], 1);
             tc::mbar_init(&a_ready[i], 4);
         }
         tc::fence_mbar_init();
     }
-    if (warp == 0) tc::tmem_alloc(tmem_slot, tc::kGroups * tc2::kColsPerGroup);
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
-    const int64_t total_groups = (int64_t)gridDim.x * tc::kGroups;
+    const int64_t total_groups = (int64_t)gridDim.x * G;
 
-    if (g >= tc::kGroups) {
-        // ===== MMA issuer warps: warp 16 + q serves group q =====
-        const int q = warp - tc::kGroups * (tc::kGroupThreads / 32);
+    if (g >= G) {
+        // ===== MMA issuer warps: warp 4G + q serves group q =====
+        const int q = warp - G * (tc::kGroupThreads / 32);
         const uint32_t b_addr = tc::smem_u32(b_tile);
         const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
                        bq2 = tc2::slice_desc(b_addr + 2048), bq3 = tc2::slice_desc(b_addr + 3072);
-        const uint32_t gc = tmem_base + q * tc2::kColsPerGroup;
-        uint32_t aph = 0;                              // bit b: parity of a_ready[q][b]
-        for (int64_t blk = (int64_t)blockIdx.x * tc::kGroups + q; blk < nblocks; blk += total_groups) {
+        uint32_t aph = 0;                              // bit s: parity of a_ready[q][s]
+        int st = 0;
+        for (int64_t blk = (int64_t)blockIdx.x * G + q; blk < nblocks; blk += total_groups) {
             for (int k = 0; k < a.g.G; ++k) {
-                const int b = k & 1;
-                tc::mbar_wait(&a_ready[2 * q + b], (aph >> b) & 1u);
-                aph ^= 1u << b;
+                tc::mbar_wait(&a_ready[q * S + st], (aph >> st) & 1u);
+                aph ^= 1u << st;
                 __syncwarp();
                 tc::fence_after();
                 if (lane == 0) {
-                    const uint32_t a_t = gc + b * 32, d_t = gc + 64 + b * 32;
+                    const uint32_t a_t = tmem_base + Cfg::a_col(q, st);
+                    const uint32_t d_t = tmem_base + Cfg::d_col(q, st);
                     tc2::mma_ts(d_t, a_t + 0, bq0, 0);
                     tc2::mma_ts(d_t, a_t + 8, bq0, 1);
                     tc2::mma_ts(d_t, a_t + 16, bq1, 1);
                     tc2::mma_ts(d_t, a_t + 0, bq2, 1);
                     tc2::mma_ts(d_t, a_t + 16, bq3, 1);
-                    tc::mma_commit(&mbars[2 * q + b]);
+                    tc::mma_commit(&d_ready[q * S + st]);
                 }
                 __syncwarp();
+                st = st + 1 == S ? 0 : st + 1;
             }
         }
     } else {
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t gcol = tmem_base + g * tc2::kColsPerGroup;   // + lane bits where needed
-    // zero the never-written tail (columns 20-23) of both A buffers of this lane
-    tc2::tmem_st_zero4(gcol + lane_off + 20);
-    tc2::tmem_st_zero4(gcol + lane_off + 32 + 20);
+    // zero the never-written tail (columns 20-23) of every A stage of this lane
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) tc2::tmem_st_zero4(tmem_base + lane_off + Cfg::a_col(g, s2) + 20);
     tc2::tmem_st_wait();
 
     float2 wo2[9];
 #pragma unroll
     for (int o = 0; o < 9; ++o) wo2[o] = make_float2(net.wo[2 * o], net.wo[2 * o + 1]);
-    uint32_t phase = 0;                        // bit b: parity of d_ready[g][b]
+    uint32_t phase = 0;                        // bit s: parity of d_ready[g][s]
     int clamps[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) clamps[l] = 0;
     const int member = t & 1;
+    int st_build = 0, st_epi = 0;              // stage of the next build / epilogue
 
-    for (int64_t blk = (int64_t)blockIdx.x * tc::kGroups + g; blk < nblocks; blk += total_groups) {
+    for (int64_t blk = (int64_t)blockIdx.x * G + g; blk < nblocks; blk += total_groups) {
         const int64_t pl = blk * tc::kPairsPerBlock + (t >> 1);
         const bool live = pl < a.P;
         int i = 0, j = 1;
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
 #pragma unroll
         for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; }
 
-        for (int k = 0; k <= a.g.G; ++k) {
+        for (int k = 0; k < a.g.G + S - 1; ++k) {
             if (k < a.g.G) {
                 // ---- 1. this lane's A row for config k, straight into TMEM ----
                 const float4 *kq = reinterpret_cast<const float4 *>(kt + (size_t)k * ROW32);
@@ -259,23 +271,25 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
                 }
                 w[18] = 0x3C003C00u;   // (1.0h, 1.0h)
                 w[19] = 0u;
-                tc2::tmem_st20(gcol + lane_off + (k & 1) * 32, w);
+                tc2::tmem_st20(tmem_base + lane_off + Cfg::a_col(g, st_build), w);
                 tc2::tmem_st_wait();
                 // order this warp's TMEM stores (and its earlier TMEM loads of the
-                // same D buffer) before the issuer's MMA, then signal A(k) ready
+                // same D stage) before the issuer's MMA, then signal A(k) ready
                 tc::fence_before();
                 __syncwarp();
-                if (lane == 0) tc2::mbar_arrive(&a_ready[2 * g + (k & 1)]);
+                if (lane == 0) tc2::mbar_arrive(&a_ready[g * S + st_build]);
+                st_build = st_build + 1 == S ? 0 : st_build + 1;
             }
-            // ---- 3. epilogue of config k-1 ----
-            if (k >= 1) {
-                const int c = k - 1, b = c & 1;
-                tc::mbar_wait(&mbars[2 * g + b], (phase >> b) & 1u);
+            // ---- 2. epilogue of config k-(S-1) ----
+            if (k >= S - 1) {
+                const int c = k - (S - 1);
+                tc::mbar_wait(&d_ready[g * S + st_epi], (phase >> st_epi) & 1u);
                 __syncwarp();
-                phase ^= 1u << b;
+                phase ^= 1u << st_epi;
                 tc::fence_after();
                 float z[HD];
-                tc::tmem_ld18(gcol + lane_off + 64 + b * 32, z);
+                tc::tmem_ld18(tmem_base + lane_off + Cfg::d_col(g, st_epi), z);
+                st_epi = st_epi + 1 == S ? 0 : st_epi + 1;
                 float2 y2 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int o = 0; o < 9; ++o)
@@ -338,14 +352,14 @@ __global__ void __launch_bounds__(kTc2Threads, 1)
     __syncthreads();
     if (warp == 0) {
         tc::fence_after();
-        tc::tmem_dealloc(tmem_base, tc::kGroups * tc2::kColsPerGroup);
+        tc::tmem_dealloc(tmem_base, 512);
     }
 }
 
-inline size_t tc2_smem_bytes(int G) {
+inline size_t tc2_smem_bytes(int n_grid) {
     size_t b = (size_t)tc2::kBBytes;
-    b += 2 * (size_t)G * ROW32 * sizeof(float) + (size_t)G * sizeof(uint32_t);
+    b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 4 * tc::kGroups * sizeof(uint64_t) + 16;
+    b += 2 * 16 * sizeof(uint64_t) + 16;
     return b;
 }

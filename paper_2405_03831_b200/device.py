@@ -117,7 +117,9 @@ class SweepPlan:
             raise ValidationError(f"pair range [{pair_begin}, {pair_end}) outside [0, {P_all})")
         self.n, self.grid, self.rel_eps = n, grid, float(rel_eps)
         kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT,
-                 "tcgen05_smem": nat.KERNEL_TCGEN05_SMEM_A}
+                 "tcgen05_smem": nat.KERNEL_TCGEN05_SMEM_A,
+                 # (compute groups, pipeline stages) variants of the TMEM-A screen
+                 "tcgen05_g4s2": 0x142, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
