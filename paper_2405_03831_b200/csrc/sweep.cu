@@ -554,7 +554,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int 
     if (smem > 227 * 1024) return CS_ERR_ARG;
     // (compute groups, pipeline stages) of the TMEM-A screen; CS_KERNEL_TCGEN05
     // uses the measured best, 0x1GS kinds select a variant for tuning
-    int G = 3, S = 3;
+    int G = 4, S = 2;
     if ((kind & 0xF00) == 0x100) { G = (kind >> 4) & 0xF; S = kind & 0xF; }
     auto go = [&](auto kern, int groups, int threads) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
