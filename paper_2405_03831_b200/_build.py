@@ -50,7 +50,8 @@ def _run(cmd, verbose: bool) -> None:
 def build_sweep(force: bool = False, verbose: bool = True) -> str:
     out = os.path.join(HERE, "libcosched_b200.so")
     src = os.path.join(CSRC, "sweep.cu")
-    deps = [src, os.path.join(INCLUDE, "cosched_b200.h")]
+    deps = [src, os.path.join(INCLUDE, "cosched_b200.h")] + [
+        os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     if force or _stale(out, deps):
         _run([_nvcc(), *NVCC_FLAGS, src, "-o", out], verbose)
     return out

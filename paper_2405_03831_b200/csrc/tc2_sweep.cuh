@@ -71,6 +71,25 @@ __device__ __forceinline__ void tmem_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// {lo half = a, hi half = b}: round toward zero with ReLU / round to nearest with ReLU
+__device__ __forceinline__ uint32_t cvt_rz_relu(float a, float b) {
+    uint32_t r;
+    asm("cvt.rz.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+__device__ __forceinline__ uint32_t cvt_rn_relu(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    unsigned long long r, x = *reinterpret_cast<unsigned long long *>(&a),
+                          y = *reinterpret_cast<unsigned long long *>(&b);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    return *reinterpret_cast<float2 *>(&r);
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
@@ -226,6 +245,7 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
     for (int64_t blk = (int64_t)blockIdx.x * G + g; blk < nblocks; blk += total_groups) {
         const int64_t pl = blk * tc::kPairsPerBlock + (t >> 1);
         const bool live = pl < a.P;
+        const int live_i = live ? 1 : 0;
         int i = 0, j = 1;
         if (live) pair_of(a.p_begin + pl, a.n, i, j);
         const int self = member ? j : i, other = member ? i : j;
@@ -256,16 +276,16 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
                                       make_float2(q2.x, q2.y), make_float2(q2.z, q2.w),
                                       make_float2(q3.x, q3.y), make_float2(q3.z, q3.w),
                                       make_float2(q4.x, q4.y)};
+                // ReLU + split in three packed steps per pair: hi = rz(relu z) <= relu z,
+                // so lo = z - hi is >= 0 whenever z >= 0 and is clamped to 0 by the
+                // second relu conversion when z < 0 (then hi = 0 as well).
                 uint32_t w[20];
 #pragma unroll
                 for (int v = 0; v < 9; ++v) {
-                    float2 z = tc2::add2(p2[v], kr[v]);
-                    z.x = fmaxf(z.x, 0.f);
-                    z.y = fmaxf(z.y, 0.f);
-                    const uint32_t hw = tc::pack_half2(z.x, z.y);
-                    const float2 back = tc::unpack_half2(hw);
-                    const float2 lo = tc2::add2(z, make_float2(-back.x, -back.y));
-                    const uint32_t lw = tc::pack_half2(lo.x, lo.y);
+                    const float2 z = tc2::add2(p2[v], kr[v]);
+                    const uint32_t hw = tc2::cvt_rz_relu(z.x, z.y);
+                    const float2 lo = tc2::sub2(z, tc::unpack_half2(hw));
+                    const uint32_t lw = tc2::cvt_rn_relu(lo.x, lo.y);
                     if (v < 8) { w[v] = hw; w[8 + v] = lw; }
                     else { w[16] = hw; w[17] = lw; }
                 }
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
                     if (L == 1 || ((m >> l) & 1u)) {
-                        clamps[l] += live ? cl : 0;
+                        clamps[l] += cl & live_i;
                         if (tt < best[l]) { second[l] = best[l]; best[l] = tt; idx[l] = c; }
                         else second[l] = fminf(second[l], tt);
                     }
