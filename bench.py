@@ -321,8 +321,10 @@ def run_ours(args):
                        "parallelism": f"pair shards x{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tf,
                          "unit": "TFLOP/s", "frac": achieved_tflops / tf, "traffic": None,
-                         "kernel": "k_sweep_tc (tcgen05)" if args.kernel == "tcgen05" else
-                                   "k_sweep (SIMT fp32)", "kernel_ms": sweep_avg,
+                         "kernel": {"tcgen05": "k_sweep_tc2<L,4,2> (tcgen05, A in TMEM)",
+                                    "simt": "k_sweep (SIMT fp32)",
+                                    "tcgen05_smem": "k_sweep_tc (tcgen05, A in SMEM)"}.get(
+                                        args.kernel, args.kernel), "kernel_ms": sweep_avg,
                          "flops_per_unit": FLOPS_PER_UNIT, "units_per_launch": units_local,
                          "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
                          "kernel_share_of_step": sweep_avg / (total_ms / args.steps)},

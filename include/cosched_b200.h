@@ -170,6 +170,26 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
                      double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                      unsigned long long *d_clamps, int kernel_kind, void *stream);
 
+/* The two halves of cs_pair_sweep_ex, for callers that overlap cs_solo with
+ * the screen (the screen does not read solo results):
+ *   cs_pair_screen    fp32 / tensor-core screen; leaves per (pair, budget) the
+ *                     screened first-index winner in out.corun_grid_index (or
+ *                     -2 when the runner-up is within rel_eps) and the
+ *                     screened value in out.weight (scratch); counts co-run
+ *                     floor clamps into d_clamps.
+ *   cs_pair_finalize  exact fp64 re-evaluation of each screened winner, the
+ *                     co-run / time-share decision, solo clamp accounting,
+ *                     and queueing of the ambiguous ones for cs_resolve. */
+int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                   const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+                   double rel_eps, cs_pair_out out, unsigned long long *d_clamps,
+                   int kernel_kind, void *stream);
+int cs_pair_finalize(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                     cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, void *stream);
+
 int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                const double *d_base_time, const double *d_solo_time, int64_t pair_begin,
                int64_t pair_end, cs_pair_out out, const int64_t *d_queue,

@@ -165,6 +165,11 @@ __device__ __forceinline__ double corun64(const cs_tables &t, const Head64P &net
     return t1 > t2 ? t1 : t2;
 }
 
+// ---- screened record (screen kernels) -> exact record (k_finalize) --------
+// The screens leave, per (pair, budget), the fp32-screened first-index winner
+// in corun_grid_index (or CS_SCREEN_AMBIGUOUS when the runner-up is within
+// rel_eps) and the screened value in weight (scratch until k_finalize).
+constexpr int32_t CS_SCREEN_AMBIGUOUS = -2;
 // ---- shared by both screens ----------------------------------------------
 struct SweepArgs {
     cs_tables t;
@@ -180,6 +185,14 @@ struct SweepArgs {
     unsigned long long *clamps;
     uint32_t *trace;         // debug builds (CS_TC_TRACE): per-thread progress, host-mapped
 };
+
+__device__ __forceinline__ void write_screened(const SweepArgs &a, int l, int64_t pl, float best,
+                                               float second, int idx) {
+    const int64_t o = (int64_t)l * a.P + pl;
+    const bool ambiguous = !(second > best * (1.0f + a.eps));
+    a.out.corun_grid_index[o] = ambiguous ? CS_SCREEN_AMBIGUOUS : idx;
+    a.out.weight[o] = (double)best;
+}
 
 __device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
     float h[HD];
@@ -212,55 +225,52 @@ __device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
+// One thread per (row, hidden unit): rows are the N apps (A and B partials),
+// then the G configs (K1 and K2, b1 folded), then the S solo splits (KS).
+// The first W2_TILE_ELEMS threads also write the fp16 B operands.
 __global__ void k_tables(const __grid_constant__ Net64P net, const double *__restrict__ feats,
                          int n, const GridP g, const cs_tables t) {
-    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid < W2_TILE_ELEMS / 2) write_b_tile(net, t.w2_tile, (int)tid);
     else if (tid < W2_TILE_ELEMS) write_b_slices(net, t.w2_tile + W2_TILE_ELEMS / 2, (int)tid - W2_TILE_ELEMS / 2);
-    const int64_t rows = (int64_t)n + g.G + g.S;
-    for (int64_t r = tid; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t items = ((int64_t)n + g.G + g.S) * HD;
+    for (int64_t e = tid; e < items; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / HD;
+        const int h = (int)(e % HD);
         if (r < n) {
-            double x1[NF], x2[NF];
             const double *f = feats + r * NF;
+            double sa = 0.0, sb = 0.0;
 #pragma unroll
             for (int k = 0; k < NF; ++k) {
-                x1[k] = clip01(f[k] / net.bounds[k]);
-                x2[k] = clip01(f[k] / net.bounds[NF + k]);
+                sa = fma(clip01(f[k] / net.bounds[k]), net.w1[h * IN + 4 + k], sa);
+                sb = fma(clip01(f[k] / net.bounds[NF + k]), net.w1[h * IN + 4 + NF + k], sb);
             }
-            for (int h = 0; h < HD; ++h) {
-                double sa = 0.0, sb = 0.0;
+            t.app_a64[r * HD + h] = sa;
+            t.app_b64[r * HD + h] = sb;
+            t.app_a32[r * ROW32 + h] = (float)sa;
+            t.app_b32[r * ROW32 + h] = (float)sb;
+            if (h < 2) t.app_a32[r * ROW32 + 18 + h] = t.app_b32[r * ROW32 + 18 + h] = 0.f;
+        } else if (r < (int64_t)n + g.G) {
+            const int64_t c = r - n;
+            double s1 = 0.0, s2 = 0.0;
 #pragma unroll
-                for (int k = 0; k < NF; ++k) {
-                    sa = fma(x1[k], net.w1[h * IN + 4 + k], sa);
-                    sb = fma(x2[k], net.w1[h * IN + 4 + NF + k], sb);
-                }
-                t.app_a64[r * HD + h] = sa;
-                t.app_b64[r * HD + h] = sb;
-                t.app_a32[r * ROW32 + h] = (float)sa;
-                t.app_b32[r * ROW32 + h] = (float)sb;
+            for (int k = 0; k < 4; ++k) {
+                s1 = fma(g.knob1[c * 4 + k], net.w1[h * IN + k], s1);
+                s2 = fma(g.knob2[c * 4 + k], net.w1[h * IN + k], s2);
             }
-            t.app_a32[r * ROW32 + 18] = t.app_a32[r * ROW32 + 19] = 0.f;
-            t.app_b32[r * ROW32 + 18] = t.app_b32[r * ROW32 + 19] = 0.f;
+            s1 = s1 + net.b1[h];
+            s2 = s2 + net.b1[h];
+            t.knob1_64[c * HD + h] = s1;
+            t.knob2_64[c * HD + h] = s2;
+            t.knob1_32[c * ROW32 + h] = (float)s1;
+            t.knob2_32[c * ROW32 + h] = (float)s2;
+            if (h < 2) t.knob1_32[c * ROW32 + 18 + h] = t.knob2_32[c * ROW32 + 18 + h] = 0.f;
         } else {
-            const bool solo = r >= (int64_t)n + g.G;
-            const int64_t c = solo ? r - n - g.G : r - n;
-            const int nviews = solo ? 1 : 2;
-            for (int v = 0; v < nviews; ++v) {
-                const double *kn = (solo ? g.solo_knob : (v == 0 ? g.knob1 : g.knob2)) + c * 4;
-                double kx[4] = {kn[0], kn[1], kn[2], kn[3]};
-                double *o64 = solo ? t.solo64 + c * HD
-                                   : (v == 0 ? t.knob1_64 : t.knob2_64) + c * HD;
-                float *o32 = solo ? nullptr : (v == 0 ? t.knob1_32 : t.knob2_32) + c * ROW32;
-                for (int h = 0; h < HD; ++h) {
-                    double s = 0.0;
+            const int64_t c = r - n - g.G;
+            double s1 = 0.0;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) s = fma(kx[k], net.w1[h * IN + k], s);
-                    s = s + net.b1[h];
-                    o64[h] = s;
-                    if (o32) o32[h] = (float)s;
-                }
-                if (o32) o32[18] = o32[19] = 0.f;
-            }
+            for (int k = 0; k < 4; ++k) s1 = fma(g.solo_knob[c * 4 + k], net.w1[h * IN + k], s1);
+            t.solo64[c * HD + h] = s1 + net.b1[h];
         }
     }
 }
@@ -301,8 +311,7 @@ __global__ void k_solo(const cs_tables t, const GridP g, const double *__restric
 
 template <int L>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
-                                                         const __grid_constant__ Net32P net,
-                                                         const __grid_constant__ Head64P net64) {
+                                                         const __grid_constant__ Net32P net) {
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int S = 1 << a.log2s;
     const int64_t pl = gt >> a.log2s;          // local pair index
@@ -369,29 +378,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
     }
 
     if (!live || s != 0) return;
-#pragma unroll 1
-    for (int l = 0; l < L; ++l) {
-        if (a.solo_clamps)
-            atomicAdd(a.clamps + l, (unsigned long long)(a.solo_clamps[(size_t)l * a.n + i] +
-                                                         a.solo_clamps[(size_t)l * a.n + j]));
-        const int64_t o = (int64_t)l * a.P + pl;
-        const bool ambiguous = !(second[l] > best[l] * (1.0f + a.eps));
-        if (ambiguous) {
-            uint32_t q = atomicAdd(a.qcount, 1u);
-            a.queue[q] = (pl << 4) | l;
-            continue;
-        }
-        const int c = idx[l];
-        const double co = corun64(a.t, net64, a.base_time, i, j, c);
-        const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
-        const bool chosen = co <= solo;                       // hwopt.py:86
-        a.out.corun_grid_index[o] = c;
-        a.out.corun_time[o] = co;
-        a.out.corun_chosen[o] = chosen;
-        a.out.weight[o] = chosen ? co : solo;
-        float gap = (float)(fabs(co - (double)best[l]) / co);
-        atomicMax(a.qcount + 1, __float_as_uint(gap));
-    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) write_screened(a, l, pl, best[l], second[l], idx[l]);
 }
 
 // ---- k_resolve: exact fp64 argmin for queued (pair, budget) ---------------
@@ -439,6 +427,66 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
             a.out.corun_chosen[o] = chosen;
             a.out.weight[o] = chosen ? best : solo;
         }
+    }
+}
+
+// ---- k_finalize: exact fp64 record of every screened (pair, budget) -------
+// Re-evaluates the screened winner in fp64 (bit-identical to the oracle),
+// takes the co-run / time-share decision against the solo pair sum
+// (hwopt.py:77-87, estimator.py:168-178), adds the solo clamps the reference
+// counts per pair, and queues the ambiguous ones for k_resolve.
+struct FinalizeArgs {
+    cs_tables t;
+    const double *base_time, *solo_time;
+    const int32_t *solo_clamps;
+    int32_t n, L;
+    int64_t p_begin, P;
+    cs_pair_out out;
+    int64_t *queue;
+    uint32_t *qcount;
+    unsigned long long *clamps;
+};
+
+__global__ void __launch_bounds__(128) k_finalize(const FinalizeArgs a,
+                                                  const __grid_constant__ Head64P net64) {
+    const int64_t total = (int64_t)a.L * a.P;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float gap_max = 0.f;
+    unsigned long long solo_cl[CS_MAX_BUDGETS] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e - threadIdx.x < total;
+         e += stride) {
+        if (e >= total) continue;                  // keep whole warps in the loop
+        const int l = (int)(e / a.P);
+        const int64_t pl = e - (int64_t)l * a.P;
+        int i, j;
+        pair_of(a.p_begin + pl, a.n, i, j);
+        if (a.solo_clamps)
+            solo_cl[l] += a.solo_clamps[(size_t)l * a.n + i] + a.solo_clamps[(size_t)l * a.n + j];
+        const int c = a.out.corun_grid_index[e];
+        if (c == CS_SCREEN_AMBIGUOUS || c < 0) {
+            const uint32_t q = atomicAdd(a.qcount, 1u);
+            a.queue[q] = (pl << 4) | l;
+            continue;
+        }
+        const double screened = a.out.weight[e];
+        const double co = corun64(a.t, net64, a.base_time, i, j, c);
+        const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
+        const bool chosen = co <= solo;                          // hwopt.py:86
+        a.out.corun_time[e] = co;
+        a.out.corun_chosen[e] = chosen;
+        a.out.weight[e] = chosen ? co : solo;
+        gap_max = fmaxf(gap_max, (float)(fabs(co - screened) / co));
+    }
+    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 16));
+    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 8));
+    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 4));
+    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 2));
+    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 1));
+    if ((threadIdx.x & 31) == 0 && gap_max > 0.f) atomicMax(a.qcount + 1, __float_as_uint(gap_max));
+    for (int l = 0; l < a.L; ++l) {
+        unsigned long long v = solo_cl[l];
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.clamps + l, v);
     }
 }
 
@@ -530,12 +578,11 @@ int choose_log2_slices(int64_t P, int G) {
 }
 
 template <int L>
-int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int kind,
-                 cudaStream_t st) {
+int launch_sweep(const SweepArgs &a, const Net32P &net, int kind, cudaStream_t st) {
     if (kind == CS_KERNEL_SIMT) {
         const int64_t threads = a.P << a.log2s;
         const int64_t blocks = (threads + kSweepThreads - 1) / kSweepThreads;
-        k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net, n64);
+        k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net);
         return CS_OK;
     }
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
@@ -547,7 +594,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int 
         if (cudaFuncSetAttribute(k_sweep_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess)
             return CS_ERR_CUDA;
-        k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, n64);
+        k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net);
         return CS_OK;
     }
     const size_t smem = tc2_smem_bytes(a.g.G);
@@ -562,7 +609,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &n64, int 
             return CS_ERR_CUDA;
         int64_t c = (nblocks + groups - 1) / groups;
         if (c > sm_count()) c = sm_count();
-        kern<<<(unsigned)c, threads, smem, st>>>(a, net, n64);
+        kern<<<(unsigned)c, threads, smem, st>>>(a, net);
         return CS_OK;
     };
     if (G == 4 && S == 2) return go(k_sweep_tc2<L, 4, 2>, 4, Tc2Cfg<4, 2>::kThreads);
@@ -632,9 +679,10 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
     if (rc) return rc;
     GridP g = grid_params(d_grid);
     if (tables->n_apps != n_apps || tables->n_grid != g.G || tables->n_solo < g.S) return CS_ERR_ARG;
-    const int64_t rows = (int64_t)n_apps + g.G + g.S;
-    int64_t threads = rows > W2_TILE_ELEMS ? rows : W2_TILE_ELEMS;
+    const int64_t items = ((int64_t)n_apps + g.G + g.S) * HD;
+    int64_t threads = items > W2_TILE_ELEMS ? items : W2_TILE_ELEMS;
     int blocks = (int)((threads + 127) / 128);
+    if (blocks > sm_count() * 16) blocks = sm_count() * 16;
     k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables);
     return check_launch();
 }
@@ -653,6 +701,110 @@ int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_gri
     return check_launch();
 }
 
+int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                   const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+                   double rel_eps, cs_pair_out out, unsigned long long *d_clamps,
+                   int kernel_kind, void *stream) {
+    Net64P n64;
+    if (!net64_from(net, &n64)) return CS_ERR_ARG;
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    if (!tables || !d_base_time || !d_clamps || !out.corun_grid_index || !out.weight)
+        return CS_ERR_ARG;
+    const int64_t n = tables->n_apps;
+    const int64_t P_all = n * (n - 1) / 2;
+    if (pair_begin < 0 || pair_end > P_all || pair_begin > pair_end) return CS_ERR_ARG;
+    if (!(rel_eps > 0.0 && rel_eps < 0.1)) return CS_ERR_ARG;
+    if (pair_begin == pair_end) return CS_OK;
+
+    Net32P n32;
+    for (int k = 0; k < HD * HD; ++k) n32.w2[k] = (float)n64.w2[k];
+    for (int k = 0; k < HD; ++k) { n32.b2[k] = (float)n64.b2[k]; n32.wo[k] = (float)n64.wo[k]; }
+    n32.bo = (float)n64.bo;
+
+    SweepArgs a{};
+    a.t = *tables;
+    a.g = grid_params(d_grid);
+    a.base_time = d_base_time;
+    a.n = (int32_t)n;
+    a.p_begin = pair_begin;
+    a.P = pair_end - pair_begin;
+    a.log2s = choose_log2_slices(a.P, a.g.G);
+    a.eps = (float)rel_eps;
+    a.out = out;
+    a.clamps = d_clamps;
+    a.trace = nullptr;
+#ifdef CS_TC_TRACE
+    a.trace = (uint32_t *)getenv_ptr("CS_TC_TRACE_PTR");
+#endif
+    cudaStream_t st = (cudaStream_t)stream;
+    if (kernel_kind == CS_KERNEL_AUTO) {
+        // the fp16 split needs |h| and |W2|, |b2| inside the fp16 range; a
+        // pathological network falls back to the fp32 SIMT screen
+        double zmax = 0.0, wmax = 0.0;
+        for (int h = 0; h < HD; ++h) {
+            double r = fabs(n64.b1[h]);
+            for (int k = 0; k < IN; ++k) r += fabs(n64.w1[h * IN + k]);
+            zmax = fmax(zmax, r);
+            wmax = fmax(wmax, fabs(n64.b2[h]));
+            for (int k = 0; k < HD; ++k) wmax = fmax(wmax, fabs(n64.w2[h * HD + k]));
+        }
+        kernel_kind = (zmax < 30000.0 && wmax < 30000.0) ? CS_KERNEL_TCGEN05 : CS_KERNEL_SIMT;
+    }
+    if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
+        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100)
+        return CS_ERR_ARG;
+    int lrc;
+    switch (a.g.L) {
+        case 1: lrc = launch_sweep<1>(a, n32, kernel_kind, st); break;
+        case 2: lrc = launch_sweep<2>(a, n32, kernel_kind, st); break;
+        case 3: lrc = launch_sweep<3>(a, n32, kernel_kind, st); break;
+        case 4: lrc = launch_sweep<4>(a, n32, kernel_kind, st); break;
+        case 5: lrc = launch_sweep<5>(a, n32, kernel_kind, st); break;
+        case 6: lrc = launch_sweep<6>(a, n32, kernel_kind, st); break;
+        case 7: lrc = launch_sweep<7>(a, n32, kernel_kind, st); break;
+        case 8: lrc = launch_sweep<8>(a, n32, kernel_kind, st); break;
+        default: return CS_ERR_ARG;
+    }
+    if (lrc) return lrc;
+    return check_launch();
+}
+
+int cs_pair_finalize(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                     cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, void *stream) {
+    Net64P n64;
+    if (!net64_from(net, &n64)) return CS_ERR_ARG;
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count || !d_clamps ||
+        !out.corun_grid_index || !out.corun_time || !out.corun_chosen || !out.weight)
+        return CS_ERR_ARG;
+    const int64_t n = tables->n_apps;
+    if (pair_begin < 0 || pair_end > n * (n - 1) / 2 || pair_begin > pair_end) return CS_ERR_ARG;
+    if (pair_begin == pair_end) return CS_OK;
+    FinalizeArgs f{};
+    f.t = *tables;
+    f.base_time = d_base_time;
+    f.solo_time = d_solo_time;
+    f.solo_clamps = d_solo_clamps;
+    f.n = (int32_t)n;
+    f.L = d_grid->n_budgets;
+    f.p_begin = pair_begin;
+    f.P = pair_end - pair_begin;
+    f.out = out;
+    f.queue = d_queue;
+    f.qcount = d_queue_count;
+    f.clamps = d_clamps;
+    const int64_t total = f.P * f.L;
+    int64_t blocks = (total + 127) / 128;
+    if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+    k_finalize<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(f, head64_from(n64));
+    return check_launch();
+}
+
 int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                   const double *d_base_time, const double *d_solo_time,
                   const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
@@ -668,63 +820,11 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
                      const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
                      double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                      unsigned long long *d_clamps, int kernel_kind, void *stream) {
-    Net64P n64;
-    if (!net64_from(net, &n64)) return CS_ERR_ARG;
-    int rc = check_grid(d_grid);
+    int rc = cs_pair_screen(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
+                            d_clamps, kernel_kind, stream);
     if (rc) return rc;
-    if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count || !d_clamps ||
-        !out.corun_grid_index || !out.corun_time || !out.corun_chosen || !out.weight)
-        return CS_ERR_ARG;
-    const int64_t n = tables->n_apps;
-    const int64_t P_all = n * (n - 1) / 2;
-    if (pair_begin < 0 || pair_end > P_all || pair_begin > pair_end) return CS_ERR_ARG;
-    if (!(rel_eps > 0.0 && rel_eps < 0.1)) return CS_ERR_ARG;
-    if (pair_begin == pair_end) return CS_OK;
-
-    Net32P n32;
-    for (int k = 0; k < HD * HD; ++k) n32.w2[k] = (float)n64.w2[k];
-    for (int k = 0; k < HD; ++k) { n32.b2[k] = (float)n64.b2[k]; n32.wo[k] = (float)n64.wo[k]; }
-    n32.bo = (float)n64.bo;
-
-    SweepArgs a;
-    a.t = *tables;
-    a.g = grid_params(d_grid);
-    a.base_time = d_base_time;
-    a.solo_time = d_solo_time;
-    a.solo_clamps = d_solo_clamps;
-    a.n = (int32_t)n;
-    a.p_begin = pair_begin;
-    a.P = pair_end - pair_begin;
-    a.log2s = choose_log2_slices(a.P, a.g.G);
-    a.eps = (float)rel_eps;
-    a.out = out;
-    a.queue = d_queue;
-    a.qcount = d_queue_count;
-    a.clamps = d_clamps;
-    a.trace = nullptr;
-#ifdef CS_TC_TRACE
-    a.trace = (uint32_t *)getenv_ptr("CS_TC_TRACE_PTR");
-#endif
-    cudaStream_t st = (cudaStream_t)stream;
-    const Head64P h64 = head64_from(n64);
-    if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
-    if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
-        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100)
-        return CS_ERR_ARG;
-    int lrc;
-    switch (a.g.L) {
-        case 1: lrc = launch_sweep<1>(a, n32, h64, kernel_kind, st); break;
-        case 2: lrc = launch_sweep<2>(a, n32, h64, kernel_kind, st); break;
-        case 3: lrc = launch_sweep<3>(a, n32, h64, kernel_kind, st); break;
-        case 4: lrc = launch_sweep<4>(a, n32, h64, kernel_kind, st); break;
-        case 5: lrc = launch_sweep<5>(a, n32, h64, kernel_kind, st); break;
-        case 6: lrc = launch_sweep<6>(a, n32, h64, kernel_kind, st); break;
-        case 7: lrc = launch_sweep<7>(a, n32, h64, kernel_kind, st); break;
-        case 8: lrc = launch_sweep<8>(a, n32, h64, kernel_kind, st); break;
-        default: return CS_ERR_ARG;
-    }
-    if (lrc) return lrc;
-    return check_launch();
+    return cs_pair_finalize(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
+                            pair_begin, pair_end, out, d_queue, d_queue_count, d_clamps, stream);
 }
 
 int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,

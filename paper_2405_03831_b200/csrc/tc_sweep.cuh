@@ -192,8 +192,7 @@ __device__ void write_b_tile(const Net64P &net, uint16_t *tile, int idx) {
 
 template <int L>
 __global__ void __launch_bounds__(tc::kThreads, 1)
-    k_sweep_tc(const SweepArgs a, const __grid_constant__ Net32P net,
-               const __grid_constant__ Head64P net64) {
+    k_sweep_tc(const SweepArgs a, const __grid_constant__ Net32P net) {
     extern __shared__ __align__(1024) uint8_t smem[];
     // carve: [A tiles: 4 groups x 2 x 16 KB][B tile 4 KB][K1 | K2 fp32 G x 20][mask G][mbar 8][tmem slot]
     uint8_t *a_tiles = smem;
@@ -341,40 +340,12 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                 }
             }
         }
-        // ---- finalize this block's pairs (both member threads cooperate) ----
+        // ---- screened records (member-0 thread of each live pair) ----
+        if (live && member == 0) {
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-            if (live && member == 0 && a.solo_clamps)
-                atomicAdd(a.clamps + l, (unsigned long long)(a.solo_clamps[(size_t)l * a.n + i] +
-                                                             a.solo_clamps[(size_t)l * a.n + j]));
-            const bool ambiguous = !(second[l] > best[l] * (1.0f + a.eps));
-            const int c = idx[l];
-            // every lane reaches the shuffle (ambiguity differs across the warp's pairs)
-            const double tm64 =
-                ambiguous ? 0.0 : member_time64(a.t, net64, a.base_time, self, other, c, member);
-            const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
-            if (ambiguous) {
-                if (live && member == 0) {
-                    const uint32_t q = atomicAdd(a.qcount, 1u);
-                    a.queue[q] = (pl << 4) | l;
-                }
-                continue;
-            }
-            if (live && member == 0) {
-                const int64_t o = (int64_t)l * a.P + pl;
-                const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) +
-                                    a.solo_time[(size_t)l * a.n + j];
-                const bool chosen = co <= solo;                  // hwopt.py:86
-                a.out.corun_grid_index[o] = c;
-                a.out.corun_time[o] = co;
-                a.out.corun_chosen[o] = chosen;
-                a.out.weight[o] = chosen ? co : solo;
-                const float gap = (float)(fabs(co - (double)best[l]) / co);
-                atomicMax(a.qcount + 1, __float_as_uint(gap));
-            }
+            for (int l = 0; l < L; ++l) write_screened(a, l, pl, best[l], second[l], idx[l]);
         }
     }
-    TC_TRACE(7, 0);
     // clamp counters: one atomic per warp and budget
 #pragma unroll
     for (int l = 0; l < L; ++l) {

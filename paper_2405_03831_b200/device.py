@@ -158,7 +158,8 @@ class SweepPlan:
             ctypes.cast(_dptr(self.solo_time), nat.c_double_p),
             ctypes.cast(_dptr(self.solo_split), nat.c_int32_p),
             ctypes.cast(_dptr(self.solo_clamps), nat.c_int32_p))
-        self.launches_per_run = 4 + (grid.n_budgets if with_matrix else 0)
+        self._side = torch.cuda.Stream(self.device)
+        self.launches_per_run = 5 + (grid.n_budgets if with_matrix else 0)
 
     # ------------------------------------------------------------------
     def launch(self, d_features: torch.Tensor, d_base_time: torch.Tensor,
@@ -176,30 +177,38 @@ class SweepPlan:
         if not (d_features.is_contiguous() and d_base_time.is_contiguous()):
             raise ValidationError("features and base_time must be contiguous")
         lib, dev = self.lib, self.device
-        st = _stream_handle(dev)
+        cur = torch.cuda.current_stream(dev)
+        st = cur.cuda_stream
         self.counters.zero_()
         self.clamps.zero_()
         tref = ctypes.byref(self.tables)
         nat.check(lib.cs_build_tables(self.net.ref(), _dptr(d_features), n, self.dgrid.ref(),
                                       tref, st), "cs_build_tables")
+        # solo splits run on a side stream, concurrently with the pair screen
+        # (the screen does not read them; cs_pair_finalize does)
+        self._side.wait_stream(cur)
         nat.check(lib.cs_solo(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                              self.solo_out, st), "cs_solo")
+                              self.solo_out, self._side.cuda_stream), "cs_solo")
         if self.P == 0:
+            cur.wait_stream(self._side)
             return
         cnt = _dptr(self.counters)
         if sweep_events is not None:
-            sweep_events[0].record()
-        nat.check(lib.cs_pair_sweep_ex(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                                       _dptr(self.solo_time), _dptr(self.solo_clamps),
-                                       self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
-                                       _dptr(self.queue), cnt, _dptr(self.clamps),
-                                       self.kernel_kind, st), "cs_pair_sweep")
+            sweep_events[0].record(cur)
+        nat.check(lib.cs_pair_screen(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
+                                     self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
+                                     _dptr(self.clamps), self.kernel_kind, st), "cs_pair_screen")
         if sweep_events is not None:
-            sweep_events[1].record()
+            sweep_events[1].record(cur)
+        cur.wait_stream(self._side)
+        nat.check(lib.cs_pair_finalize(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
+                                       _dptr(self.solo_time), _dptr(self.solo_clamps),
+                                       self.pair_begin, self.pair_end, self.pair_out,
+                                       _dptr(self.queue), cnt, _dptr(self.clamps), st),
+                  "cs_pair_finalize")
         nat.check(lib.cs_resolve(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                                 _dptr(self.solo_time),
-                                 self.pair_begin, self.pair_end, self.pair_out, _dptr(self.queue),
-                                 cnt, st), "cs_resolve")
+                                 _dptr(self.solo_time), self.pair_begin, self.pair_end,
+                                 self.pair_out, _dptr(self.queue), cnt, st), "cs_resolve")
         if self.matrix is not None:
             self.scatter(st)
 
