@@ -142,6 +142,18 @@ __device__ __forceinline__ double head64c(const Head64P &net, const double (&z)[
     return y > 0.0 ? y : 0.0;
 }
 
+// Stage the fp64 head weights in shared memory: 324+ distinct fp64 constants
+// overflow the per-SM constant cache, while a shared-memory copy is read with
+// broadcast LDS (every lane of a warp reads the same address).
+__device__ __forceinline__ const Head64P &stage_head64(const Head64P &param, Head64P &sm) {
+    const double *src = reinterpret_cast<const double *>(&param);
+    double *dst = reinterpret_cast<double *>(&sm);
+    for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / sizeof(double)); i += blockDim.x)
+        dst[i] = src[i];
+    __syncthreads();
+    return sm;
+}
+
 // floor(pred) x T of one member of pair (self, other) under config c
 // (member 0: K1 / view hc, member 1: K2 / reversed partitions)
 __device__ __forceinline__ double member_time64(const cs_tables &t, const Head64P &net,
@@ -228,28 +240,39 @@ __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v >
 // One thread per (row, hidden unit): rows are the N apps (A and B partials),
 // then the G configs (K1 and K2, b1 folded), then the S solo splits (KS).
 // The first W2_TILE_ELEMS threads also write the fp16 B operands.
+// One warp per row -- the N apps (A and B partials), then the G configs (K1,
+// K2, b1 folded), then the S solo splits (KS) -- with lane h < 18 producing
+// hidden unit h; for app rows lane k first normalizes counter k (the fp64
+// divisions happen once per app).  Threads below W2_TILE_ELEMS also write the
+// fp16 B operands of the tensor-core screens.
 __global__ void k_tables(const __grid_constant__ Net64P net, const double *__restrict__ feats,
                          int n, const GridP g, const cs_tables t) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid < W2_TILE_ELEMS / 2) write_b_tile(net, t.w2_tile, (int)tid);
     else if (tid < W2_TILE_ELEMS) write_b_slices(net, t.w2_tile + W2_TILE_ELEMS / 2, (int)tid - W2_TILE_ELEMS / 2);
-    const int64_t items = ((int64_t)n + g.G + g.S) * HD;
-    for (int64_t e = tid; e < items; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / HD;
-        const int h = (int)(e % HD);
+    const int lane = threadIdx.x & 31;
+    const int h = lane < HD ? lane : HD - 1;
+    const int64_t rows = (int64_t)n + g.G + g.S;
+    for (int64_t r = tid >> 5; r < rows; r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         if (r < n) {
-            const double *f = feats + r * NF;
+            const double f = lane < NF ? feats[r * NF + lane] : 0.0;
+            const double x1 = lane < NF ? clip01(f / net.bounds[lane]) : 0.0;
+            const double x2 = lane < NF ? clip01(f / net.bounds[NF + lane]) : 0.0;
             double sa = 0.0, sb = 0.0;
 #pragma unroll
             for (int k = 0; k < NF; ++k) {
-                sa = fma(clip01(f[k] / net.bounds[k]), net.w1[h * IN + 4 + k], sa);
-                sb = fma(clip01(f[k] / net.bounds[NF + k]), net.w1[h * IN + 4 + NF + k], sb);
+                sa = fma(__shfl_sync(0xffffffffu, x1, k), net.w1[h * IN + 4 + k], sa);
+                sb = fma(__shfl_sync(0xffffffffu, x2, k), net.w1[h * IN + 4 + NF + k], sb);
             }
-            t.app_a64[r * HD + h] = sa;
-            t.app_b64[r * HD + h] = sb;
-            t.app_a32[r * ROW32 + h] = (float)sa;
-            t.app_b32[r * ROW32 + h] = (float)sb;
-            if (h < 2) t.app_a32[r * ROW32 + 18 + h] = t.app_b32[r * ROW32 + 18 + h] = 0.f;
+            if (lane < HD) {
+                t.app_a64[r * HD + h] = sa;
+                t.app_b64[r * HD + h] = sb;
+                t.app_a32[r * ROW32 + h] = (float)sa;
+                t.app_b32[r * ROW32 + h] = (float)sb;
+            } else if (lane < ROW32) {
+                t.app_a32[r * ROW32 + lane] = 0.f;
+                t.app_b32[r * ROW32 + lane] = 0.f;
+            }
         } else if (r < (int64_t)n + g.G) {
             const int64_t c = r - n;
             double s1 = 0.0, s2 = 0.0;
@@ -260,17 +283,21 @@ __global__ void k_tables(const __grid_constant__ Net64P net, const double *__res
             }
             s1 = s1 + net.b1[h];
             s2 = s2 + net.b1[h];
-            t.knob1_64[c * HD + h] = s1;
-            t.knob2_64[c * HD + h] = s2;
-            t.knob1_32[c * ROW32 + h] = (float)s1;
-            t.knob2_32[c * ROW32 + h] = (float)s2;
-            if (h < 2) t.knob1_32[c * ROW32 + 18 + h] = t.knob2_32[c * ROW32 + 18 + h] = 0.f;
+            if (lane < HD) {
+                t.knob1_64[c * HD + h] = s1;
+                t.knob2_64[c * HD + h] = s2;
+                t.knob1_32[c * ROW32 + h] = (float)s1;
+                t.knob2_32[c * ROW32 + h] = (float)s2;
+            } else if (lane < ROW32) {
+                t.knob1_32[c * ROW32 + lane] = 0.f;
+                t.knob2_32[c * ROW32 + lane] = 0.f;
+            }
         } else {
             const int64_t c = r - n - g.G;
             double s1 = 0.0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) s1 = fma(g.solo_knob[c * 4 + k], net.w1[h * IN + k], s1);
-            t.solo64[c * HD + h] = s1 + net.b1[h];
+            if (lane < HD) t.solo64[c * HD + h] = s1 + net.b1[h];
         }
     }
 }
@@ -279,7 +306,9 @@ __global__ void k_tables(const __grid_constant__ Net64P net, const double *__res
 // One warp per (budget, app); lane s evaluates split s (a budget has <= 32
 // splits: 17 on the 6.25 W grid), then a first-index argmin over the warp.
 __global__ void k_solo(const cs_tables t, const GridP g, const double *__restrict__ base_time,
-                       int n, cs_solo_out out, const __grid_constant__ Head64P net) {
+                       int n, cs_solo_out out, const __grid_constant__ Head64P net_param) {
+    __shared__ Head64P net_sm;
+    const Head64P &net = stage_head64(net_param, net_sm);
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= (int64_t)n * g.L) return;
@@ -395,7 +424,9 @@ struct ResolveArgs {
 };
 
 __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
-                                                 const __grid_constant__ Head64P net64) {
+                                                 const __grid_constant__ Head64P net_param) {
+    __shared__ Head64P net_sm;
+    const Head64P &net64 = stage_head64(net_param, net_sm);
     const uint32_t count = *a.qcount;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -448,7 +479,9 @@ struct FinalizeArgs {
 };
 
 __global__ void __launch_bounds__(128) k_finalize(const FinalizeArgs a,
-                                                  const __grid_constant__ Head64P net64) {
+                                                  const __grid_constant__ Head64P net_param) {
+    __shared__ Head64P net_sm;
+    const Head64P &net64 = stage_head64(net_param, net_sm);
     const int64_t total = (int64_t)a.L * a.P;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     float gap_max = 0.f;
@@ -679,7 +712,7 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
     if (rc) return rc;
     GridP g = grid_params(d_grid);
     if (tables->n_apps != n_apps || tables->n_grid != g.G || tables->n_solo < g.S) return CS_ERR_ARG;
-    const int64_t items = ((int64_t)n_apps + g.G + g.S) * HD;
+    const int64_t items = ((int64_t)n_apps + g.G + g.S) * 32;
     int64_t threads = items > W2_TILE_ELEMS ? items : W2_TILE_ELEMS;
     int blocks = (int)((threads + 127) / 128);
     if (blocks > sm_count() * 16) blocks = sm_count() * 16;
