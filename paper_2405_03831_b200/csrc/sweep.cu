@@ -123,20 +123,28 @@ Head64P head64_from(const Net64P &n) {
 }
 
 __device__ __forceinline__ double head64c(const Head64P &net, const double (&z)[HD]) {
-    double acc[HD];
+    double h1[HD];
 #pragma unroll
-    for (int o = 0; o < HD; ++o) acc[o] = 0.0;
-#pragma unroll
-    for (int k = 0; k < HD; ++k) {
-        const double hk = z[k] > 0.0 ? z[k] : 0.0;
-#pragma unroll
-        for (int o = 0; o < HD; ++o) acc[o] = fma(hk, net.w2[o * HD + k], acc[o]);
-    }
+    for (int k = 0; k < HD; ++k) h1[k] = z[k] > 0.0 ? z[k] : 0.0;
     double y = 0.0;
+    // three output units at a time: 3 independent accumulation chains in flight
+    // without hoisting all 324 weights into registers
+#pragma unroll 1
+    for (int o = 0; o < HD; o += 3) {
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+        const double *w0 = net.w2 + o * HD, *w1r = w0 + HD, *w2r = w1r + HD;
 #pragma unroll
-    for (int o = 0; o < HD; ++o) {
-        const double a2 = acc[o] + net.b2[o];
-        y = fma(a2 > 0.0 ? a2 : 0.0, net.wo[o], y);
+        for (int k = 0; k < HD; ++k) {
+            acc0 = fma(h1[k], w0[k], acc0);
+            acc1 = fma(h1[k], w1r[k], acc1);
+            acc2 = fma(h1[k], w2r[k], acc2);
+        }
+        acc0 = acc0 + net.b2[o];
+        acc1 = acc1 + net.b2[o + 1];
+        acc2 = acc2 + net.b2[o + 2];
+        y = fma(acc0 > 0.0 ? acc0 : 0.0, net.wo[o], y);
+        y = fma(acc1 > 0.0 ? acc1 : 0.0, net.wo[o + 1], y);
+        y = fma(acc2 > 0.0 ? acc2 : 0.0, net.wo[o + 2], y);
     }
     y = y + net.bo;
     return y > 0.0 ? y : 0.0;
