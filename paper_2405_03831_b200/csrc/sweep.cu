@@ -122,22 +122,50 @@ Head64P head64_from(const Net64P &n) {
     return h;
 }
 
-__device__ __forceinline__ double head64c(const Head64P &net, const double (&z)[HD]) {
+__device__ __forceinline__ double head64c(const Head64P &net_in, const double (&z)[HD]) {
+    // Launder the weight pointer so the compiler re-reads the (shared-memory)
+    // weights per evaluation instead of hoisting 324 doubles into registers
+    // across calls; k-outer / o-inner keeps 18 independent fp64 chains in
+    // flight (FP64 latency x throughput needs that much ILP), and every chain
+    // still sums over k in the oracle's order (bit-identical results).
+    const Head64P *netp = &net_in;
+    asm volatile("" : "+l"(netp));
+    const Head64P &net = *netp;
+    double acc[HD];
+#pragma unroll
+    for (int o = 0; o < HD; ++o) acc[o] = 0.0;
+#pragma unroll
+    for (int k = 0; k < HD; ++k) {
+        const double hk = z[k] > 0.0 ? z[k] : 0.0;
+#pragma unroll
+        for (int o = 0; o < HD; ++o) acc[o] = fma(hk, net.w2[o * HD + k], acc[o]);
+    }
+    double y = 0.0;
+#pragma unroll
+    for (int o = 0; o < HD; ++o) {
+        const double a2 = acc[o] + net.b2[o];
+        y = fma(a2 > 0.0 ? a2 : 0.0, net.wo[o], y);
+    }
+    y = y + net.bo;
+    return y > 0.0 ? y : 0.0;
+}
+
+// Register-lean variant (three output units per pass) for kernels whose
+// per-thread work is a handful of heads (k_solo): same summation order.
+__device__ __forceinline__ double head64_lean(const Head64P &net, const double (&z)[HD]) {
     double h1[HD];
 #pragma unroll
     for (int k = 0; k < HD; ++k) h1[k] = z[k] > 0.0 ? z[k] : 0.0;
     double y = 0.0;
-    // three output units at a time: 3 independent accumulation chains in flight
-    // without hoisting all 324 weights into registers
 #pragma unroll 1
     for (int o = 0; o < HD; o += 3) {
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-        const double *w0 = net.w2 + o * HD, *w1r = w0 + HD, *w2r = w1r + HD;
+        const double *r0 = net.w2 + o * HD, *r1 = r0 + HD, *r2 = r1 + HD;
 #pragma unroll
         for (int k = 0; k < HD; ++k) {
-            acc0 = fma(h1[k], w0[k], acc0);
-            acc1 = fma(h1[k], w1r[k], acc1);
-            acc2 = fma(h1[k], w2r[k], acc2);
+            acc0 = fma(h1[k], r0[k], acc0);
+            acc1 = fma(h1[k], r1[k], acc1);
+            acc2 = fma(h1[k], r2[k], acc2);
         }
         acc0 = acc0 + net.b2[o];
         acc1 = acc1 + net.b2[o + 1];
@@ -328,7 +356,7 @@ __global__ void k_solo(const cs_tables t, const GridP g, const double *__restric
         double z[HD];
 #pragma unroll
         for (int h = 0; h < HD; ++h) z[h] = t.app_a64[(size_t)a * HD + h] + t.solo64[(size_t)(s0 + s) * HD + h];
-        double y = head64c(net, z);
+        double y = head64_lean(net, z);
         if (y < FLOOR) { ++clamp; y = FLOOR; }
         const double tt = y * base_time[a];
         if (tt < best) { best = tt; arg = s; }
@@ -433,13 +461,15 @@ struct ResolveArgs {
 
 __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
                                                  const __grid_constant__ Head64P net_param) {
+    // One block per queued (pair, budget); thread c evaluates configs c, c+128, ...
+    // in fp64, then a block-wide first-index argmin (ties -> smallest index).
     __shared__ Head64P net_sm;
+    __shared__ double red_v[4];
+    __shared__ int red_i[4];
     const Head64P &net64 = stage_head64(net_param, net_sm);
     const uint32_t count = *a.qcount;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t q = warp; q < count; q += nwarps) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t q = blockIdx.x; q < count; q += gridDim.x) {
         const int64_t e = a.queue[q];
         const int64_t pl = e >> 4;
         const int l = (int)(e & 15);
@@ -447,17 +477,21 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
         pair_of(a.p_begin + pl, a.n, i, j);
         double best = INFINITY;
         int arg = INT_MAX;
-        for (int c = lane; c < a.g.G; c += 32) {
+        for (int c = threadIdx.x; c < a.g.G; c += blockDim.x) {
             if (!((__ldg(a.g.mask + c) >> l) & 1u)) continue;
-            double tt = corun64(a.t, net64, a.base_time, i, j, c);
-            if (tt < best) { best = tt; arg = c; }          // ascending c per lane: first index
+            const double tt = corun64(a.t, net64, a.base_time, i, j, c);
+            if (tt < best) { best = tt; arg = c; }          // ascending c per thread
         }
         for (int off = 16; off; off >>= 1) {
-            double ob = __shfl_xor_sync(0xffffffffu, best, off);
-            int oi = __shfl_xor_sync(0xffffffffu, arg, off);
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, arg, off);
             if (ob < best || (ob == best && oi < arg)) { best = ob; arg = oi; }
         }
-        if (lane == 0) {
+        if (lane == 0) { red_v[warp] = best; red_i[warp] = arg; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+                if (red_v[w] < best || (red_v[w] == best && red_i[w] < arg)) { best = red_v[w]; arg = red_i[w]; }
             const int64_t o = (int64_t)l * a.P + pl;
             const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
             const bool chosen = arg != INT_MAX && best <= solo;
@@ -466,6 +500,7 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
             a.out.corun_chosen[o] = chosen;
             a.out.weight[o] = chosen ? best : solo;
         }
+        __syncthreads();
     }
 }
 
@@ -889,8 +924,8 @@ int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_
     a.out = out;
     a.queue = d_queue;
     a.qcount = d_queue_count;
-    // the queue length lives on the device: launch one resident wave, grid-stride
-    k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a, head64_from(n64));
+    // the queue length lives on the device: launch a resident grid, block-stride
+    k_resolve<<<sm_count() * 8, 128, 0, (cudaStream_t)stream>>>(a, head64_from(n64));
     return check_launch();
 }
 
