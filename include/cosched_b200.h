@@ -144,56 +144,54 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
 int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
             const double *d_base_time, cs_solo_out out, void *stream);
 
-/* `net` (host) is passed again because the fp32 screen keeps W2 in the kernel
- * parameter bank.  Screens every (pair, config) of the shard in fp32, keeps per (pair, budget)
- * the first-index minimum and the runner-up value; when the runner-up is more
- * than `rel_eps` above the minimum the winner is re-evaluated in fp64 and the
- * record finalized, otherwise the (pair, budget) is queued for cs_resolve,
- * which re-scans it in fp64 (exact first-index argmin).  d_queue needs
- * L * (pair_end - pair_begin) int64 slots.
- * d_clamps (L x u64, zeroed by the caller) accumulates floor clamps exactly as
- * the reference's clamp_stats counts them over build_graph (2 per co-run
- * config + 2 x S solo per pair).  d_queue_count holds two zeroed u32: [0] the
- * queue length, [1] the largest relative gap seen between an fp32-screened
- * winner and its fp64 re-evaluation (float bits) -- a runtime check that the
- * screen error stays far below rel_eps. */
-int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-                  const double *d_base_time,
-                  const double *d_solo_time, const int32_t *d_solo_clamps, int64_t pair_begin,
-                  int64_t pair_end, double rel_eps, cs_pair_out out, int64_t *d_queue,
-                  uint32_t *d_queue_count, unsigned long long *d_clamps, void *stream);
+/* The pair sweep is three stream-ordered steps (cs_solo may run concurrently
+ * with the first two; only cs_pair_decide reads the solo results):
+ *
+ *   cs_pair_screen  screens every (pair, config) of the shard -- on the tensor
+ *                   cores by default (CS_KERNEL_*) -- keeping per (pair,
+ *                   budget) the first-index minimum and the runner-up.  When
+ *                   the runner-up is more than rel_eps above the minimum the
+ *                   winner is re-evaluated in fp64 (corun_grid_index /
+ *                   corun_time final); otherwise corun_grid_index = -2 and the
+ *                   (pair, budget) is appended to d_queue (needs L * P int64
+ *                   slots).  d_queue_count holds two zeroed u32: [0] the queue
+ *                   length, [1] the largest relative gap seen between a
+ *                   screened winner and its fp64 value (float bits).  Co-run
+ *                   floor clamps accumulate in d_clamps (L x u64, zeroed).
+ *   cs_resolve      exact fp64 first-index argmin for every queued entry.
+ *   cs_pair_decide  co-run vs time-share per (pair, budget) against the solo
+ *                   pair sum, adds the solo clamps the reference counts per
+ *                   pair (so d_clamps ends equal to clamp_stats over
+ *                   build_graph), and optionally scatters the winning times
+ *                   into d_w (L x N x N, zeroed by the caller).
+ *
+ * `net` (host) is passed to the kernels that need it by value (parameter
+ * bank).  cs_pair_sweep[_ex] = screen + resolve + decide without d_w. */
+int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                   const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+                   double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                   unsigned long long *d_clamps, int kernel_kind, void *stream);
 
-/* cs_pair_sweep with an explicit screen kernel (CS_KERNEL_*). */
+int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+               const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+               void *stream);
+
+int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32_t *d_solo_clamps,
+                   int32_t n_apps, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
+                   unsigned long long *d_clamps, double *d_w, void *stream);
+
+int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                  const double *d_base_time, const double *d_solo_time,
+                  const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                  double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                  unsigned long long *d_clamps, void *stream);
+
 int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, const double *d_solo_time,
                      const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
                      double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                      unsigned long long *d_clamps, int kernel_kind, void *stream);
-
-/* The two halves of cs_pair_sweep_ex, for callers that overlap cs_solo with
- * the screen (the screen does not read solo results):
- *   cs_pair_screen    fp32 / tensor-core screen; leaves per (pair, budget) the
- *                     screened first-index winner in out.corun_grid_index (or
- *                     -2 when the runner-up is within rel_eps) and the
- *                     screened value in out.weight (scratch); counts co-run
- *                     floor clamps into d_clamps.
- *   cs_pair_finalize  exact fp64 re-evaluation of each screened winner, the
- *                     co-run / time-share decision, solo clamp accounting,
- *                     and queueing of the ambiguous ones for cs_resolve. */
-int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-                   const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-                   double rel_eps, cs_pair_out out, unsigned long long *d_clamps,
-                   int kernel_kind, void *stream);
-int cs_pair_finalize(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-                     const double *d_base_time, const double *d_solo_time,
-                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                     cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
-                     unsigned long long *d_clamps, void *stream);
-
-int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-               const double *d_base_time, const double *d_solo_time, int64_t pair_begin,
-               int64_t pair_end, cs_pair_out out, const int64_t *d_queue,
-               const uint32_t *d_queue_count, void *stream);
 
 /* W[i*N+j] = W[j*N+i] = weight of budget `budget`; the caller zeroes W. */
 int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,

@@ -95,17 +95,15 @@ SWEEP_SYMBOLS = {
     "cs_pair_screen": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
                                       ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_int64,
                                       ctypes.c_int64, ctypes.c_double, CsPairOut, ctypes.c_void_p,
-                                      ctypes.c_int, ctypes.c_void_p]),
-    "cs_pair_finalize": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
-                                        ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_void_p,
-                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, CsPairOut,
-                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                        ctypes.c_void_p]),
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                      ctypes.c_void_p]),
     "cs_resolve": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
-                                  ctypes.POINTER(CsGrid),
-                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                  ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_int64, CsPairOut, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p]),
+    "cs_pair_decide": (ctypes.c_int, [ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, CsPairOut,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_scatter_weights": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_forward_rows": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_int64,

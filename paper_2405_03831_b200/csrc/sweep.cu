@@ -204,6 +204,18 @@ __device__ __forceinline__ double member_time64(const cs_tables &t, const Head64
     return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
 }
 
+__device__ __forceinline__ double member_time64_lean(const cs_tables &t, const Head64P &net,
+                                                     const double *__restrict__ base_time,
+                                                     int self, int other, int c, int member) {
+    double z[HD];
+    const double *as = t.app_a64 + (size_t)self * HD, *bo = t.app_b64 + (size_t)other * HD;
+    const double *kk = (member ? t.knob2_64 : t.knob1_64) + (size_t)c * HD;
+#pragma unroll
+    for (int h = 0; h < HD; ++h) z[h] = (__ldg(as + h) + __ldg(bo + h)) + __ldg(kk + h);
+    const double y = head64_lean(net, z);
+    return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
+}
+
 // CoRunTime of one config for pair (i, j): max over members (estimator.py:127-129)
 __device__ __forceinline__ double corun64(const cs_tables &t, const Head64P &net,
                                           const double *__restrict__ base_time, int i, int j,
@@ -213,10 +225,9 @@ __device__ __forceinline__ double corun64(const cs_tables &t, const Head64P &net
     return t1 > t2 ? t1 : t2;
 }
 
-// ---- screened record (screen kernels) -> exact record (k_finalize) --------
-// The screens leave, per (pair, budget), the fp32-screened first-index winner
-// in corun_grid_index (or CS_SCREEN_AMBIGUOUS when the runner-up is within
-// rel_eps) and the screened value in weight (scratch until k_finalize).
+// ---- screened record -------------------------------------------------------
+// The screens leave, per (pair, budget), either the winner (index + its fp64
+// CoRunTime) or CS_SCREEN_AMBIGUOUS plus a queue entry for k_resolve.
 constexpr int32_t CS_SCREEN_AMBIGUOUS = -2;
 // ---- shared by both screens ----------------------------------------------
 struct SweepArgs {
@@ -234,12 +245,25 @@ struct SweepArgs {
     uint32_t *trace;         // debug builds (CS_TC_TRACE): per-thread progress, host-mapped
 };
 
-__device__ __forceinline__ void write_screened(const SweepArgs &a, int l, int64_t pl, float best,
-                                               float second, int idx) {
+__device__ __forceinline__ bool screen_ambiguous(const SweepArgs &a, float best, float second) {
+    return !(second > best * (1.0f + a.eps));
+}
+
+// ambiguous (pair, budget): leave it to k_resolve
+__device__ __forceinline__ void push_ambiguous(const SweepArgs &a, int l, int64_t pl) {
     const int64_t o = (int64_t)l * a.P + pl;
-    const bool ambiguous = !(second > best * (1.0f + a.eps));
-    a.out.corun_grid_index[o] = ambiguous ? CS_SCREEN_AMBIGUOUS : idx;
-    a.out.weight[o] = (double)best;
+    a.out.corun_grid_index[o] = CS_SCREEN_AMBIGUOUS;
+    const uint32_t q = atomicAdd(a.qcount, 1u);
+    a.queue[q] = (pl << 4) | l;
+}
+
+// certain winner: its exact fp64 CoRunTime (+ the screen-error monitor)
+__device__ __forceinline__ void write_winner(const SweepArgs &a, int l, int64_t pl, int idx,
+                                             double co, float best) {
+    const int64_t o = (int64_t)l * a.P + pl;
+    a.out.corun_grid_index[o] = idx;
+    a.out.corun_time[o] = co;
+    atomicMax(a.qcount + 1, __float_as_uint((float)(fabs(co - (double)best) / co)));
 }
 
 __device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
@@ -376,7 +400,10 @@ __global__ void k_solo(const cs_tables t, const GridP g, const double *__restric
 
 template <int L>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
-                                                         const __grid_constant__ Net32P net) {
+                                                         const __grid_constant__ Net32P net,
+                                                         const __grid_constant__ Head64P net_param) {
+    __shared__ Head64P net_sm;
+    const Head64P &net64 = stage_head64(net_param, net_sm);
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int S = 1 << a.log2s;
     const int64_t pl = gt >> a.log2s;          // local pair index
@@ -443,8 +470,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
     }
 
     if (!live || s != 0) return;
-#pragma unroll
-    for (int l = 0; l < L; ++l) write_screened(a, l, pl, best[l], second[l], idx[l]);
+#pragma unroll 1
+    for (int l = 0; l < L; ++l) {
+        if (screen_ambiguous(a, best[l], second[l])) { push_ambiguous(a, l, pl); continue; }
+        const double co = fmax(member_time64_lean(a.t, net64, a.base_time, i, j, idx[l], 0),
+                               member_time64_lean(a.t, net64, a.base_time, j, i, idx[l], 1));
+        write_winner(a, l, pl, idx[l], co, best[l]);
+    }
 }
 
 // ---- k_resolve: exact fp64 argmin for queued (pair, budget) ---------------
@@ -493,76 +525,62 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
             for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
                 if (red_v[w] < best || (red_v[w] == best && red_i[w] < arg)) { best = red_v[w]; arg = red_i[w]; }
             const int64_t o = (int64_t)l * a.P + pl;
-            const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
-            const bool chosen = arg != INT_MAX && best <= solo;
             a.out.corun_grid_index[o] = arg == INT_MAX ? -1 : arg;
-            a.out.corun_time[o] = best;
-            a.out.corun_chosen[o] = chosen;
-            a.out.weight[o] = chosen ? best : solo;
+            a.out.corun_time[o] = arg == INT_MAX ? INFINITY : best;
         }
         __syncthreads();
     }
 }
 
-// ---- k_finalize: exact fp64 record of every screened (pair, budget) -------
-// Re-evaluates the screened winner in fp64 (bit-identical to the oracle),
-// takes the co-run / time-share decision against the solo pair sum
-// (hwopt.py:77-87, estimator.py:168-178), adds the solo clamps the reference
-// counts per pair, and queues the ambiguous ones for k_resolve.
-struct FinalizeArgs {
-    cs_tables t;
-    const double *base_time, *solo_time;
+// ---- k_decide: co-run vs time-share per (pair, budget) (hwopt.py:77-87) ----
+// corun_time is final here (screen winner re-evaluated in fp64, or k_resolve);
+// the solo pair sum is (0.0 + t_i) + t_j (estimator.py:168-178).  Also adds the
+// solo-split clamps the reference counts per pair and, when W is given,
+// scatters the winning time into the symmetric N x N matrix of budget l.
+struct DecideArgs {
+    const double *solo_time;
     const int32_t *solo_clamps;
     int32_t n, L;
     int64_t p_begin, P;
     cs_pair_out out;
-    int64_t *queue;
-    uint32_t *qcount;
     unsigned long long *clamps;
+    double *W;               // L x N x N or null
 };
 
-__global__ void __launch_bounds__(128) k_finalize(const FinalizeArgs a,
-                                                  const __grid_constant__ Head64P net_param) {
-    __shared__ Head64P net_sm;
-    const Head64P &net64 = stage_head64(net_param, net_sm);
+__global__ void __launch_bounds__(256) k_decide(const DecideArgs a) {
     const int64_t total = (int64_t)a.L * a.P;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    float gap_max = 0.f;
-    unsigned long long solo_cl[CS_MAX_BUDGETS] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e - threadIdx.x < total;
-         e += stride) {
-        if (e >= total) continue;                  // keep whole warps in the loop
+    unsigned long long cl[CS_MAX_BUDGETS] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
         const int l = (int)(e / a.P);
         const int64_t pl = e - (int64_t)l * a.P;
         int i, j;
         pair_of(a.p_begin + pl, a.n, i, j);
-        if (a.solo_clamps)
-            solo_cl[l] += a.solo_clamps[(size_t)l * a.n + i] + a.solo_clamps[(size_t)l * a.n + j];
-        const int c = a.out.corun_grid_index[e];
-        if (c == CS_SCREEN_AMBIGUOUS || c < 0) {
-            const uint32_t q = atomicAdd(a.qcount, 1u);
-            a.queue[q] = (pl << 4) | l;
-            continue;
-        }
-        const double screened = a.out.weight[e];
-        const double co = corun64(a.t, net64, a.base_time, i, j, c);
-        const double solo = (0.0 + a.solo_time[(size_t)l * a.n + i]) + a.solo_time[(size_t)l * a.n + j];
-        const bool chosen = co <= solo;                          // hwopt.py:86
-        a.out.corun_time[e] = co;
+        const double *st = a.solo_time + (size_t)l * a.n;
+        const double solo = (0.0 + st[i]) + st[j];
+        const double co = a.out.corun_time[e];
+        const bool chosen = a.out.corun_grid_index[e] >= 0 && co <= solo;   // hwopt.py:86
+        const double w = chosen ? co : solo;
         a.out.corun_chosen[e] = chosen;
-        a.out.weight[e] = chosen ? co : solo;
-        gap_max = fmaxf(gap_max, (float)(fabs(co - screened) / co));
+        a.out.weight[e] = w;
+        if (a.W) {
+            double *Wl = a.W + (size_t)l * a.n * a.n;
+            Wl[(size_t)i * a.n + j] = w;
+            Wl[(size_t)j * a.n + i] = w;
+        }
+        if (a.solo_clamps) {
+#pragma unroll
+            for (int b = 0; b < CS_MAX_BUDGETS; ++b)
+                if (b == l) cl[b] += a.solo_clamps[(size_t)l * a.n + i] + a.solo_clamps[(size_t)l * a.n + j];
+        }
     }
-    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 16));
-    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 8));
-    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 4));
-    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 2));
-    gap_max = fmaxf(gap_max, __shfl_xor_sync(0xffffffffu, gap_max, 1));
-    if ((threadIdx.x & 31) == 0 && gap_max > 0.f) atomicMax(a.qcount + 1, __float_as_uint(gap_max));
-    for (int l = 0; l < a.L; ++l) {
-        unsigned long long v = solo_cl[l];
+    if (!a.solo_clamps) return;
+#pragma unroll
+    for (int b = 0; b < CS_MAX_BUDGETS; ++b) {
+        if (b >= a.L) break;
+        unsigned long long v = cl[b];
         for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.clamps + l, v);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.clamps + b, v);
     }
 }
 
@@ -654,11 +672,12 @@ int choose_log2_slices(int64_t P, int G) {
 }
 
 template <int L>
-int launch_sweep(const SweepArgs &a, const Net32P &net, int kind, cudaStream_t st) {
+int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int kind,
+                 cudaStream_t st) {
     if (kind == CS_KERNEL_SIMT) {
         const int64_t threads = a.P << a.log2s;
         const int64_t blocks = (threads + kSweepThreads - 1) / kSweepThreads;
-        k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net);
+        k_sweep<L><<<(unsigned)blocks, kSweepThreads, 0, st>>>(a, net, h64);
         return CS_OK;
     }
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
@@ -670,7 +689,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, int kind, cudaStream_t s
         if (cudaFuncSetAttribute(k_sweep_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess)
             return CS_ERR_CUDA;
-        k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net);
+        k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, h64);
         return CS_OK;
     }
     const size_t smem = tc2_smem_bytes(a.g.G);
@@ -685,7 +704,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, int kind, cudaStream_t s
             return CS_ERR_CUDA;
         int64_t c = (nblocks + groups - 1) / groups;
         if (c > sm_count()) c = sm_count();
-        kern<<<(unsigned)c, threads, smem, st>>>(a, net);
+        kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
         return CS_OK;
     };
     if (G == 4 && S == 2) return go(k_sweep_tc2<L, 4, 2>, 4, Tc2Cfg<4, 2>::kThreads);
@@ -779,13 +798,14 @@ int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_gri
 
 int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                    const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-                   double rel_eps, cs_pair_out out, unsigned long long *d_clamps,
-                   int kernel_kind, void *stream) {
+                   double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                   unsigned long long *d_clamps, int kernel_kind, void *stream) {
     Net64P n64;
     if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
     if (rc) return rc;
-    if (!tables || !d_base_time || !d_clamps || !out.corun_grid_index || !out.weight)
+    if (!tables || !d_base_time || !d_clamps || !out.corun_grid_index || !out.corun_time ||
+        !d_queue || !d_queue_count)
         return CS_ERR_ARG;
     const int64_t n = tables->n_apps;
     const int64_t P_all = n * (n - 1) / 2;
@@ -808,12 +828,15 @@ int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid
     a.log2s = choose_log2_slices(a.P, a.g.G);
     a.eps = (float)rel_eps;
     a.out = out;
+    a.queue = d_queue;
+    a.qcount = d_queue_count;
     a.clamps = d_clamps;
     a.trace = nullptr;
 #ifdef CS_TC_TRACE
     a.trace = (uint32_t *)getenv_ptr("CS_TC_TRACE_PTR");
 #endif
     cudaStream_t st = (cudaStream_t)stream;
+    const Head64P h64 = head64_from(n64);
     if (kernel_kind == CS_KERNEL_AUTO) {
         // the fp16 split needs |h| and |W2|, |b2| inside the fp16 range; a
         // pathological network falls back to the fp32 SIMT screen
@@ -832,52 +855,45 @@ int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid
         return CS_ERR_ARG;
     int lrc;
     switch (a.g.L) {
-        case 1: lrc = launch_sweep<1>(a, n32, kernel_kind, st); break;
-        case 2: lrc = launch_sweep<2>(a, n32, kernel_kind, st); break;
-        case 3: lrc = launch_sweep<3>(a, n32, kernel_kind, st); break;
-        case 4: lrc = launch_sweep<4>(a, n32, kernel_kind, st); break;
-        case 5: lrc = launch_sweep<5>(a, n32, kernel_kind, st); break;
-        case 6: lrc = launch_sweep<6>(a, n32, kernel_kind, st); break;
-        case 7: lrc = launch_sweep<7>(a, n32, kernel_kind, st); break;
-        case 8: lrc = launch_sweep<8>(a, n32, kernel_kind, st); break;
+        case 1: lrc = launch_sweep<1>(a, n32, h64, kernel_kind, st); break;
+        case 2: lrc = launch_sweep<2>(a, n32, h64, kernel_kind, st); break;
+        case 3: lrc = launch_sweep<3>(a, n32, h64, kernel_kind, st); break;
+        case 4: lrc = launch_sweep<4>(a, n32, h64, kernel_kind, st); break;
+        case 5: lrc = launch_sweep<5>(a, n32, h64, kernel_kind, st); break;
+        case 6: lrc = launch_sweep<6>(a, n32, h64, kernel_kind, st); break;
+        case 7: lrc = launch_sweep<7>(a, n32, h64, kernel_kind, st); break;
+        case 8: lrc = launch_sweep<8>(a, n32, h64, kernel_kind, st); break;
         default: return CS_ERR_ARG;
     }
     if (lrc) return lrc;
     return check_launch();
 }
 
-int cs_pair_finalize(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-                     const double *d_base_time, const double *d_solo_time,
-                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                     cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
-                     unsigned long long *d_clamps, void *stream) {
-    Net64P n64;
-    if (!net64_from(net, &n64)) return CS_ERR_ARG;
+int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32_t *d_solo_clamps,
+                   int32_t n_apps, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
+                   unsigned long long *d_clamps, double *d_w, void *stream) {
     int rc = check_grid(d_grid);
     if (rc) return rc;
-    if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count || !d_clamps ||
-        !out.corun_grid_index || !out.corun_time || !out.corun_chosen || !out.weight)
+    if (!d_solo_time || n_apps < 2 || !out.corun_grid_index || !out.corun_time ||
+        !out.corun_chosen || !out.weight || (d_solo_clamps && !d_clamps))
         return CS_ERR_ARG;
-    const int64_t n = tables->n_apps;
-    if (pair_begin < 0 || pair_end > n * (n - 1) / 2 || pair_begin > pair_end) return CS_ERR_ARG;
+    if (pair_begin < 0 || pair_end > (int64_t)n_apps * (n_apps - 1) / 2 || pair_begin > pair_end)
+        return CS_ERR_ARG;
     if (pair_begin == pair_end) return CS_OK;
-    FinalizeArgs f{};
-    f.t = *tables;
-    f.base_time = d_base_time;
-    f.solo_time = d_solo_time;
-    f.solo_clamps = d_solo_clamps;
-    f.n = (int32_t)n;
-    f.L = d_grid->n_budgets;
-    f.p_begin = pair_begin;
-    f.P = pair_end - pair_begin;
-    f.out = out;
-    f.queue = d_queue;
-    f.qcount = d_queue_count;
-    f.clamps = d_clamps;
-    const int64_t total = f.P * f.L;
-    int64_t blocks = (total + 127) / 128;
-    if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
-    k_finalize<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(f, head64_from(n64));
+    DecideArgs d{};
+    d.solo_time = d_solo_time;
+    d.solo_clamps = d_solo_clamps;
+    d.n = n_apps;
+    d.L = d_grid->n_budgets;
+    d.p_begin = pair_begin;
+    d.P = pair_end - pair_begin;
+    d.out = out;
+    d.clamps = d_clamps;
+    d.W = d_w;
+    const int64_t total = d.P * d.L;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
+    k_decide<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d);
     return check_launch();
 }
 
@@ -897,27 +913,29 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
                      double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                      unsigned long long *d_clamps, int kernel_kind, void *stream) {
     int rc = cs_pair_screen(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
-                            d_clamps, kernel_kind, stream);
+                            d_queue, d_queue_count, d_clamps, kernel_kind, stream);
     if (rc) return rc;
-    return cs_pair_finalize(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
-                            pair_begin, pair_end, out, d_queue, d_queue_count, d_clamps, stream);
+    rc = cs_resolve(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
+                    d_queue_count, stream);
+    if (rc) return rc;
+    return cs_pair_decide(d_grid, d_solo_time, d_solo_clamps, tables->n_apps, pair_begin,
+                          pair_end, out, d_clamps, nullptr, stream);
 }
 
 int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-               const double *d_base_time, const double *d_solo_time, int64_t pair_begin,
-               int64_t pair_end, cs_pair_out out, const int64_t *d_queue,
-               const uint32_t *d_queue_count, void *stream) {
+               const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+               void *stream) {
     Net64P n64;
     if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
     if (rc) return rc;
-    if (!tables || !d_base_time || !d_solo_time || !d_queue || !d_queue_count) return CS_ERR_ARG;
+    if (!tables || !d_base_time || !d_queue || !d_queue_count) return CS_ERR_ARG;
     if (pair_begin == pair_end) return CS_OK;
-    ResolveArgs a;
+    ResolveArgs a{};
     a.t = *tables;
     a.g = grid_params(d_grid);
     a.base_time = d_base_time;
-    a.solo_time = d_solo_time;
     a.n = tables->n_apps;
     a.p_begin = pair_begin;
     a.P = pair_end - pair_begin;
@@ -983,7 +1001,7 @@ GraphLayout graph_layout(int32_t n, const cs_grid *g) {
     L.queue = put(sizeof(int64_t) * (size_t)(nb * P));
     L.qcount = put(sizeof(uint32_t) * 2);
     L.clamps = put(sizeof(unsigned long long) * (size_t)nb);
-    L.W = put(sizeof(double) * (size_t)n * n);
+    L.W = put(sizeof(double) * (size_t)n * n * nb);
     L.total = off;
     return L;
 }
@@ -1037,17 +1055,18 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     CS_RC(cs_solo(net, &t, &dg, (const double *)(ws + L.bt), so, stream));
     cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
-    CS_RC(cs_pair_sweep(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time, so.solo_clamps, 0, P,
-                        rel_eps, po, (int64_t *)(ws + L.queue), (uint32_t *)(ws + L.qcount),
-                        (unsigned long long *)(ws + L.clamps), stream));
-    CS_RC(cs_resolve(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time, 0, P, po,
+    CS_RC(cs_pair_screen(net, &t, &dg, (const double *)(ws + L.bt), 0, P, rel_eps, po,
+                         (int64_t *)(ws + L.queue), (uint32_t *)(ws + L.qcount),
+                         (unsigned long long *)(ws + L.clamps), CS_KERNEL_AUTO, stream));
+    CS_RC(cs_resolve(net, &t, &dg, (const double *)(ws + L.bt), 0, P, po,
                      (const int64_t *)(ws + L.queue), (const uint32_t *)(ws + L.qcount), stream));
-    for (int l = 0; l < nb && h_weights; ++l) {
-        CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n, st));
-        CS_RC(cs_scatter_weights(po.weight + (size_t)l * P, n_apps, 0, P, (double *)(ws + L.W), stream));
-        CS_TRY(cudaMemcpyAsync(h_weights + (size_t)l * n * n, ws + L.W, sizeof(double) * n * n,
+    if (h_weights) CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n * nb, st));
+    CS_RC(cs_pair_decide(&dg, so.solo_time, so.solo_clamps, n_apps, 0, P, po,
+                         (unsigned long long *)(ws + L.clamps),
+                         h_weights ? (double *)(ws + L.W) : nullptr, stream));
+    if (h_weights)
+        CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
                                cudaMemcpyDeviceToHost, st));
-    }
     const size_t LP = (size_t)nb * P, LN = (size_t)nb * n;
     if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP, cudaMemcpyDeviceToHost, st));
     if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));

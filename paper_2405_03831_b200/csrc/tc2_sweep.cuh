@@ -151,7 +151,8 @@ struct Tc2Cfg {
 
 template <int L, int G, int S>
 __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
-    k_sweep_tc2(const SweepArgs a, const __grid_constant__ Net32P net) {
+    k_sweep_tc2(const SweepArgs a, const __grid_constant__ Net32P net,
+                const __grid_constant__ Head64P net_param) {
     using Cfg = Tc2Cfg<G, S>;
     extern __shared__ __align__(1024) uint8_t smem[];
     // carve: [B slices 4 KB][K1 | K2 fp32 G x 20][mask G][d_ready G*S][a_ready G*S][tmem slot]
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
         (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
     uint64_t *a_ready = d_ready + G * S;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + G * S);
+    Head64P *net64 = reinterpret_cast<Head64P *>(a_ready + G * S + 2);
 
     const int tid = threadIdx.x;
     const int g = tid / tc::kGroupThreads;     // >= G: the MMA-issuer warps
@@ -180,6 +182,8 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
         k2s[i] = a.t.knob2_32[i];
     }
     for (int i = tid; i < a.g.G; i += Cfg::kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
+    for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += Cfg::kThreads)
+        reinterpret_cast<double *>(net64)[i] = reinterpret_cast<const double *>(&net_param)[i];
     if (tid == 0) {
         for (int i = 0; i < G * S; ++i) {
             tc::mbar_init(&d_ready[i], 1);
@@ -329,10 +333,19 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
                 }
             }
         }
-        // ---- screened records (member-0 thread of each live pair) ----
-        if (live && member == 0) {
-#pragma unroll
-            for (int l = 0; l < L; ++l) write_screened(a, l, pl, best[l], second[l], idx[l]);
+        // ---- per (pair, budget): queue it, or re-evaluate the winner in fp64
+        //      (member m's thread computes member m's time; one shuffle) ----
+#pragma unroll 1
+        for (int l = 0; l < L; ++l) {
+            const bool ambiguous = screen_ambiguous(a, best[l], second[l]);
+            // every lane reaches the shuffle (ambiguity differs across the warp's pairs)
+            const double tm64 = ambiguous ? 0.0
+                : member_time64_lean(a.t, *net64, a.base_time, self, other, idx[l], member);
+            const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
+            if (live && member == 0) {
+                if (ambiguous) push_ambiguous(a, l, pl);
+                else write_winner(a, l, pl, idx[l], co, best[l]);
+            }
         }
     }
 #pragma unroll
@@ -353,6 +366,6 @@ inline size_t tc2_smem_bytes(int n_grid) {
     size_t b = (size_t)tc2::kBBytes;
     b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * 16 * sizeof(uint64_t) + 16;
+    b += 2 * 16 * sizeof(uint64_t) + 16 + sizeof(Head64P);
     return b;
 }

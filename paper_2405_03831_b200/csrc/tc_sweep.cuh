@@ -192,7 +192,8 @@ __device__ void write_b_tile(const Net64P &net, uint16_t *tile, int idx) {
 
 template <int L>
 __global__ void __launch_bounds__(tc::kThreads, 1)
-    k_sweep_tc(const SweepArgs a, const __grid_constant__ Net32P net) {
+    k_sweep_tc(const SweepArgs a, const __grid_constant__ Net32P net,
+               const __grid_constant__ Head64P net_param) {
     extern __shared__ __align__(1024) uint8_t smem[];
     // carve: [A tiles: 4 groups x 2 x 16 KB][B tile 4 KB][K1 | K2 fp32 G x 20][mask G][mbar 8][tmem slot]
     uint8_t *a_tiles = smem;
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     uint64_t *mbars = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbars + 2 * tc::kGroups);
+    Head64P *net64 = reinterpret_cast<Head64P *>(mbars + 2 * tc::kGroups + 2);
 
     const int tid = threadIdx.x;
     const int g = tid / tc::kGroupThreads;        // group
@@ -219,6 +221,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
         k2s[i] = a.t.knob2_32[i];
     }
     for (int i = tid; i < a.g.G; i += tc::kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
+    for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += tc::kThreads)
+        reinterpret_cast<double *>(net64)[i] = reinterpret_cast<const double *>(&net_param)[i];
     if (tid == 0) {
         for (int i = 0; i < 2 * tc::kGroups; ++i) tc::mbar_init(&mbars[i], 1);
         tc::fence_mbar_init();
@@ -340,10 +344,19 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                 }
             }
         }
-        // ---- screened records (member-0 thread of each live pair) ----
-        if (live && member == 0) {
-#pragma unroll
-            for (int l = 0; l < L; ++l) write_screened(a, l, pl, best[l], second[l], idx[l]);
+        // ---- per (pair, budget): queue it, or re-evaluate the winner in fp64
+        //      (member m's thread computes member m's time; one shuffle) ----
+#pragma unroll 1
+        for (int l = 0; l < L; ++l) {
+            const bool ambiguous = screen_ambiguous(a, best[l], second[l]);
+            // every lane reaches the shuffle (ambiguity differs across the warp's pairs)
+            const double tm64 = ambiguous ? 0.0
+                : member_time64_lean(a.t, *net64, a.base_time, self, other, idx[l], member);
+            const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
+            if (live && member == 0) {
+                if (ambiguous) push_ambiguous(a, l, pl);
+                else write_winner(a, l, pl, idx[l], co, best[l]);
+            }
         }
     }
     // clamp counters: one atomic per warp and budget
@@ -365,6 +378,6 @@ inline size_t tc_smem_bytes(int G) {
     size_t b = (size_t)tc::kGroups * 2 * tc::kTileBytes + tc::kBBytes;
     b += 2 * (size_t)G * ROW32 * sizeof(float) + (size_t)G * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * tc::kGroups * sizeof(uint64_t) + 16;
+    b += 2 * tc::kGroups * sizeof(uint64_t) + 16 + sizeof(Head64P);
     return b;
 }

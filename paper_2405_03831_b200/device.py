@@ -159,7 +159,7 @@ class SweepPlan:
             ctypes.cast(_dptr(self.solo_split), nat.c_int32_p),
             ctypes.cast(_dptr(self.solo_clamps), nat.c_int32_p))
         self._side = torch.cuda.Stream(self.device)
-        self.launches_per_run = 5 + (grid.n_budgets if with_matrix else 0)
+        self.launches_per_run = 6
 
     # ------------------------------------------------------------------
     def launch(self, d_features: torch.Tensor, d_base_time: torch.Tensor,
@@ -197,19 +197,20 @@ class SweepPlan:
             sweep_events[0].record(cur)
         nat.check(lib.cs_pair_screen(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
                                      self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
-                                     _dptr(self.clamps), self.kernel_kind, st), "cs_pair_screen")
+                                     _dptr(self.queue), cnt, _dptr(self.clamps), self.kernel_kind,
+                                     st), "cs_pair_screen")
         if sweep_events is not None:
             sweep_events[1].record(cur)
-        cur.wait_stream(self._side)
-        nat.check(lib.cs_pair_finalize(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                                       _dptr(self.solo_time), _dptr(self.solo_clamps),
-                                       self.pair_begin, self.pair_end, self.pair_out,
-                                       _dptr(self.queue), cnt, _dptr(self.clamps), st),
-                  "cs_pair_finalize")
         nat.check(lib.cs_resolve(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                                 _dptr(self.solo_time), self.pair_begin, self.pair_end,
-                                 self.pair_out, _dptr(self.queue), cnt, st), "cs_resolve")
-        if self.matrix is not None:
+                                 self.pair_begin, self.pair_end, self.pair_out, _dptr(self.queue),
+                                 cnt, st), "cs_resolve")
+        cur.wait_stream(self._side)
+        # decisions (+ the symmetric matrix when this plan owns the whole graph)
+        w = _dptr(self.matrix) if (self.matrix is not None and self.P == n_pairs(n)) else None
+        nat.check(lib.cs_pair_decide(self.dgrid.ref(), _dptr(self.solo_time),
+                                     _dptr(self.solo_clamps), n, self.pair_begin, self.pair_end,
+                                     self.pair_out, _dptr(self.clamps), w, st), "cs_pair_decide")
+        if self.matrix is not None and w is None:
             self.scatter(st)
 
     def scatter(self, st=None) -> None:
