@@ -202,6 +202,12 @@ int cs_forward_rows(const cs_network *net, const double *d_x, int64_t rows, doub
                     void *stream);
 
 /* --- host-buffer convenience: the whole build_graph --------------------- */
+/* Device workspace for callers without their own allocator (the ctypes binding
+ * in INTEGRATION.md): cudaMalloc / cudaFree on the current device, 256-byte
+ * aligned.  These are the only allocating calls of the ABI. */
+int cs_device_alloc(size_t bytes, void **d_out);
+int cs_device_free(void *d_ptr);
+
 size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid);
 /* h_weights: L x N x N (NULL to skip); h_pairs members: L x P host arrays
  * (NULL members skipped); h_solo members: L x N host arrays (NULL skipped);

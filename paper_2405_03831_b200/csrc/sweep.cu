@@ -1007,6 +1007,21 @@ GraphLayout graph_layout(int32_t n, const cs_grid *g) {
 }
 }  // namespace
 
+int cs_device_alloc(size_t bytes, void **d_out) {
+    if (!d_out || !bytes) return CS_ERR_ARG;
+    *d_out = nullptr;
+    if (cudaMalloc(d_out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return CS_ERR_CUDA;
+    }
+    return CS_OK;
+}
+
+int cs_device_free(void *d_ptr) {
+    if (d_ptr && cudaFree(d_ptr) != cudaSuccess) return CS_ERR_CUDA;
+    return CS_OK;
+}
+
 size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid) {
     if (n_apps < 2 || check_grid(h_grid) != CS_OK) return 0;
     return graph_layout(n_apps, h_grid).total;
