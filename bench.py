@@ -321,7 +321,8 @@ def run_ours(args):
                        "parallelism": f"pair shards x{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tf,
                          "unit": "TFLOP/s", "frac": achieved_tflops / tf, "traffic": None,
-                         "kernel": {"tcgen05": "k_sweep_tc2<L,4,2> (tcgen05, A in TMEM)",
+                         "kernel": {"tcgen05": "k_sweep_tc3<L,3,3> (tcgen05, A in TMEM, v4)",
+                                    "tcgen05_v3": "k_sweep_tc2<L,4,2> (tcgen05, A in TMEM, v3)",
                                     "simt": "k_sweep (SIMT fp32)",
                                     "tcgen05_smem": "k_sweep_tc (tcgen05, A in SMEM)"}.get(
                                         args.kernel, args.kernel), "kernel_ms": sweep_avg,
@@ -389,8 +390,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--workload", default="n256", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "tcgen05_smem", "simt", "tcgen05_g4s2", "tcgen05_g3s3",
-                             "tcgen05_g2s4"],
+    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "tcgen05_v3", "tcgen05_smem", "simt", "tcgen05_g4s2",
+                             "tcgen05_g3s3", "tcgen05_g2s4", "tcgen05_v4_g3s3",
+                             "tcgen05_v4_g4s2"] + [f"tcgen05_v4_g{g}s{s}_f{v}" for g, s in
+                                                   ((3, 3), (4, 2)) for v in range(4)],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

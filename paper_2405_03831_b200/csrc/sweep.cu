@@ -293,6 +293,7 @@ __device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&
 
 #include "tc_sweep.cuh"
 #include "tc2_sweep.cuh"
+#include "tc3_sweep.cuh"
 
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -692,10 +693,36 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
         k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, h64);
         return CS_OK;
     }
+    if (kind == CS_KERNEL_TCGEN05 || (kind & 0xF00) == 0x300) {
+        // v4 screen (tc3_sweep.cuh); 0xV3GS kinds select a (groups, stages,
+        // variant flags) instance for tuning
+        // default: 4 groups x 2 stages, per-group issuer warps, elected arrives
+        if (kind == CS_KERNEL_TCGEN05) kind = 0x3342;
+        const int G = (kind >> 4) & 0xF, S = kind & 0xF;
+        const size_t smem = tc3_smem_bytes(a.g.G);
+        if (smem > 227 * 1024) return CS_ERR_ARG;
+        auto go3 = [&](auto kern, int groups, int threads) -> int {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
+                return CS_ERR_CUDA;
+            int64_t c = (nblocks + groups - 1) / groups;
+            if (c > sm_count()) c = sm_count();
+            kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
+            return CS_OK;
+        };
+        const int V = (kind >> 12) & 0xF;
+#define CS_TC3(GG, SS, VV) \
+        if (G == GG && S == SS && V == VV) \
+            return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
+        CS_TC3(3, 3, 0) CS_TC3(3, 3, 1) CS_TC3(3, 3, 2) CS_TC3(3, 3, 3)
+        CS_TC3(4, 2, 0) CS_TC3(4, 2, 1) CS_TC3(4, 2, 2) CS_TC3(4, 2, 3)
+#undef CS_TC3
+        return CS_ERR_ARG;
+    }
     const size_t smem = tc2_smem_bytes(a.g.G);
     if (smem > 227 * 1024) return CS_ERR_ARG;
-    // (compute groups, pipeline stages) of the TMEM-A screen; CS_KERNEL_TCGEN05
-    // uses the measured best, 0x1GS kinds select a variant for tuning
+    // (compute groups, pipeline stages) variants of the v3 TMEM-A screen
+    // (tc2_sweep.cuh), selected by 0x1GS kinds for comparison
     int G = 4, S = 2;
     if ((kind & 0xF00) == 0x100) { G = (kind >> 4) & 0xF; S = kind & 0xF; }
     auto go = [&](auto kern, int groups, int threads) -> int {
@@ -851,7 +878,8 @@ int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid
         kernel_kind = (zmax < 30000.0 && wmax < 30000.0) ? CS_KERNEL_TCGEN05 : CS_KERNEL_SIMT;
     }
     if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
-        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100)
+        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100 &&
+        (kernel_kind & 0xF00) != 0x300)
         return CS_ERR_ARG;
     int lrc;
     switch (a.g.L) {

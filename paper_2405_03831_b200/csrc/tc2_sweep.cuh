@@ -16,7 +16,7 @@
 //   col 18     1.0, 1.0               (carries b2 = b2hi + b2lo)
 //   cols 19-23 0
 // B is held as four 16-wide K slices (N = 32 rows each, canonical layout):
-//   q0 = W2hi[:, 0:16]   q1 = [W2hi16 W2hi17 W2hi16 W2hi17 b2hi b2lo 0..]
+//   q0 = W2hi[:, 0:16]   q1 = [W2hi16 W2hi17 W2hi16 W2hi17 b2hi b2lo W2lo16 W2lo17 0..]
 //   q2 = W2lo[:, 0:16]   q3 = [W2lo16 W2lo17 0..]
 // and z2 = A_s0 q0 + A_s1 q0 + A_s2 q1 + A_s0 q2 + A_s2 q3 (5 MMAs, K = 16):
 // (hi + lo) W2hi + hi W2lo + b2, the same 3-term split as v2.
@@ -126,6 +126,10 @@ __device__ void write_b_slices(const Net64P &net, uint16_t *tile, int idx) {
             else if (kk == 1 || kk == 3) v = hi_of(w[17]);
             else if (kk == 4) v = hi_of(net.b2[n]);
             else if (kk == 5) v = net.b2[n] - hi_of(net.b2[n]);
+            // k 6-7 meet A column 19: zero in this kernel, (hi16, hi17) in
+            // k_sweep_tc3, which so folds the q3 term into this slice
+            else if (kk == 6) v = w[16] - hi_of(w[16]);
+            else if (kk == 7) v = w[17] - hi_of(w[17]);
         } else {  // q == 3
             if (kk == 0) v = w[16] - hi_of(w[16]);
             else if (kk == 1) v = w[17] - hi_of(w[17]);

@@ -1,0 +1,373 @@
+// tc3_sweep.cuh -- tcgen05 screen, v4: the v3 (tc2) pipeline on an instruction diet.
+//
+// Same math, TMEM map and result contract as k_sweep_tc2 (A operand in TMEM,
+// fp16 3-term split, 5 x tcgen05.mma M=128 N=32 K=16, fp32 epilogue, fp64
+// re-evaluation of the winner).  Profiling tc2 (profiles/r1a_sweep_ncu.md)
+// showed CUDA-core issue as the binding limit: 196 warp instructions per
+// (warp, config) where ~115 are the math itself.  This version removes the
+// rest:
+//   * the config loop is unrolled over the S pipeline stages, so every TMEM
+//     address, mbarrier address and phase bit is a compile-time offset;
+//   * G compute groups share ONE MMA-issuer warp (lockstep over groups), so
+//     G = 3 fits 4 warps per scheduler and 128 registers per thread;
+//   * every compute thread arrives on a_ready itself (count 128): no
+//     __syncwarp + elected arrive per config;
+//   * the MMA-issuer warps sleep in mbarrier.try_wait with a suspend-time hint
+//     instead of spinning on the issue slots the compute warps need;
+//   * the K1/K2 rows of a config are interleaved ([c][member][20]) so both
+//     member lanes of a warp read one 160-byte line;
+//   * floor clamps are counted per block and masked by `live` once per block.
+#pragma once
+
+namespace tc3 {
+
+// V bit 0: one elected arrive per warp on a_ready (count 4) instead of all
+//           128 threads arriving;
+// V bit 1: one MMA-issuer warp per group instead of one shared issuer.
+template <int G, int S, int V = 0>
+struct Cfg {
+    static constexpr bool kElected = (V & 1) != 0;
+    static constexpr bool kPerGroupIssuer = (V & 2) != 0;
+    static constexpr int kIssuers = kPerGroupIssuer ? G : 1;
+    static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
+    static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
+    __device__ static constexpr uint32_t d_col(int g, int s) { return (uint32_t)((g * S + s) * 32); }
+    __device__ static constexpr uint32_t a_col(int g, int s) {
+        return (uint32_t)(G * S * 32 + (g * S + s) * 24);
+    }
+};
+
+// try_wait with a suspend-time hint: the warp sleeps in the barrier unit
+// instead of re-issuing the probe (used by the MMA-issuer warps)
+__device__ __forceinline__ bool mbar_try_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    if (mbar_try_sleep(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_sleep(bar, parity)) {
+        if (clock64() - t0 > 4000000000LL) __trap();
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive_all(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+// tcgen05.st of the 20 live A columns as 8 + 8 + 4 (smaller register blocks
+// than one x16 leave ptxas room to store the conversions in place)
+__device__ __forceinline__ void tmem_st20_848(uint32_t taddr, const uint32_t (&w)[20]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 8),
+                 "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+                 "r"(w[15])
+                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + 16),
+                 "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19])
+                 : "memory");
+}
+
+// The 4 MMAs of one (group, config) plus the commit, issued by ONE elected
+// lane inside a single asm block that the whole (converged) warp executes:
+// no divergent branch around tcgen05.mma, so ptxas does not wrap every MMA in
+// a uniformization loop.  tools/mma_bench.cu measured 29 cycles/MMA issued
+// this way against 75+ for a `lane == 0` branch (the tensor pipe itself
+// sustains one M128 N32 K16 MMA per ~16 cycles per SM).
+//   z2 = A_s0 q0 + A_s1 q0 + A_s2 q1 + A_s0 q2
+__device__ __forceinline__ void issue_config(uint32_t d_t, uint32_t a_t, uint64_t bq0, uint64_t bq1,
+                                             uint64_t bq2, uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e, pf, pt;\n\t"
+        "setp.ne.b32 pf, %6, %6;\n\t"
+        "setp.eq.b32 pt, %6, %6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %6, pf;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %3, %6, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %4, %6, pt;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %6, pt;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%2];\n}"
+        ::"r"(d_t), "r"(a_t), "r"(tc::smem_u32(bar)), "l"(bq0), "l"(bq1), "l"(bq2), "r"(tc::kIdesc),
+          "r"(a_t + 8), "r"(a_t + 16)
+        : "memory");
+}
+
+// this thread's A row of one config (20 live 32-bit TMEM columns, layout of
+// tc2_sweep.cuh), stored into its TMEM lane
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds2(uint32_t a) {
+    float2 v;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
+// krow: 32-bit shared-window address of this member's K row (a plain
+// integer, so ptxas never re-derives the generic->shared mapping in the loop)
+__device__ __forceinline__ void build_row(const float2 (&p2)[9], uint32_t krow, uint32_t taddr) {
+    const float4 q0 = lds4(krow), q1 = lds4(krow + 16), q2 = lds4(krow + 32), q3 = lds4(krow + 48);
+    const float2 q4 = lds2(krow + 64);
+    const float2 kr[9] = {make_float2(q0.x, q0.y), make_float2(q0.z, q0.w),
+                          make_float2(q1.x, q1.y), make_float2(q1.z, q1.w),
+                          make_float2(q2.x, q2.y), make_float2(q2.z, q2.w),
+                          make_float2(q3.x, q3.y), make_float2(q3.z, q3.w), q4};
+    uint32_t w[20];
+#pragma unroll
+    for (int v = 0; v < 9; ++v) {
+        const float2 z = tc2::add2(p2[v], kr[v]);
+        const uint32_t hw = tc2::cvt_rz_relu(z.x, z.y);
+        const float2 lo = tc2::sub2(z, tc::unpack_half2(hw));
+        const uint32_t lw = tc2::cvt_rn_relu(lo.x, lo.y);
+        if (v < 8) { w[v] = hw; w[8 + v] = lw; }
+        else { w[16] = hw; w[17] = lw; }
+    }
+    w[18] = 0x3C003C00u;   // (1.0h, 1.0h): carries b2
+    w[19] = w[16];         // (hi16, hi17) again: carries W2lo[:, 16:18]
+    tmem_st20_848(taddr, w);
+    tc2::tmem_st_wait();
+    tc::fence_before();
+}
+
+// y = wo . ReLU(z2) + bo for this thread's row of one config (fp32, FFMA2)
+__device__ __forceinline__ float head_from_tmem(uint32_t taddr, const float2 (&wo2)[9], float bo) {
+    float z[HD];
+    tc::tmem_ld18(taddr, z);
+    float2 y2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int o = 0; o < 9; ++o)
+        y2 = tc2::fma2(make_float2(fmaxf(z[2 * o], 0.f), fmaxf(z[2 * o + 1], 0.f)), wo2[o], y2);
+    return (y2.x + y2.y) + bo;
+}
+
+}  // namespace tc3
+
+template <int L, int G, int S, int V>
+__global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
+    k_sweep_tc3(const SweepArgs a, const __grid_constant__ Net32P net,
+                const __grid_constant__ Head64P net_param) {
+    using C = tc3::Cfg<G, S, V>;
+    constexpr int kThreads = C::kThreads;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    // carve: [B slices 4 KB][K12: G_cfg x 2 x 20 fp32][mask G_cfg][d_ready G*S][a_ready G*S]
+    //        [tmem slot][Head64P][wo, bo fp32]
+    uint8_t *b_tile = smem;
+    float *k12 = reinterpret_cast<float *>(smem + tc2::kBBytes);
+    uint32_t *masks = reinterpret_cast<uint32_t *>(k12 + (size_t)a.g.G * 2 * ROW32);
+    uint64_t *d_ready = reinterpret_cast<uint64_t *>(
+        (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
+    uint64_t *a_ready = d_ready + G * S;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + G * S);
+    Head64P *net64 = reinterpret_cast<Head64P *>(a_ready + G * S + 2);
+    float *wo_s = reinterpret_cast<float *>(net64 + 1);          // wo[18], bo
+
+    const int tid = threadIdx.x;
+    const int g = tid / tc::kGroupThreads;     // == G: the MMA-issuer warp
+    const int t = tid % tc::kGroupThreads;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    for (int i = tid; i < tc2::kBBytes / 16; i += kThreads)
+        reinterpret_cast<uint4 *>(b_tile)[i] =
+            reinterpret_cast<const uint4 *>(a.t.w2_tile + tc::kBBytes / 2)[i];
+    for (int i = tid; i < a.g.G * ROW32; i += kThreads) {
+        const int c = i / ROW32, h = i - c * ROW32;
+        k12[(2 * c) * ROW32 + h] = a.t.knob1_32[i];
+        k12[(2 * c + 1) * ROW32 + h] = a.t.knob2_32[i];
+    }
+    for (int i = tid; i < a.g.G; i += kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
+    if (tid <= HD) wo_s[tid] = tid < HD ? net.wo[tid] : net.bo;
+    for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += kThreads)
+        reinterpret_cast<double *>(net64)[i] = reinterpret_cast<const double *>(&net_param)[i];
+    if (tid == 0) {
+        for (int i = 0; i < G * S; ++i) {
+            tc::mbar_init(&d_ready[i], 1);
+            tc::mbar_init(&a_ready[i], C::kElected ? tc::kGroupThreads / 32 : tc::kGroupThreads);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
+    const int64_t total_groups = (int64_t)gridDim.x * G;
+    const int n_cfg = a.g.G;
+
+    if (g >= G) {
+        // ===== one MMA-issuer warp serves the G groups in lockstep =====
+        // Every active group of a round sweeps the same configs in the same
+        // order, so the issuer visits (config k, group q) round-robin.
+        const uint32_t b_addr = tc::smem_u32(b_tile);
+        const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
+                       bq2 = tc2::slice_desc(b_addr + 2048);
+        uint32_t ph = 0;                               // bit q*S+s: parity of a_ready[q][s]
+        // per-group issuers: warp G*4 + q serves only group q
+        const int q_lo = C::kPerGroupIssuer ? warp - G * (tc::kGroupThreads / 32) : 0;
+        for (int64_t blk0 = (int64_t)blockIdx.x * G; blk0 < nblocks; blk0 += total_groups) {
+            const int active = nblocks - blk0 < G ? (int)(nblocks - blk0) : G;
+            const int q_hi = C::kPerGroupIssuer ? (q_lo < active ? q_lo + 1 : q_lo) : active;
+            int st = 0;
+            for (int k = 0; k < n_cfg; ++k) {
+                for (int q = q_lo; q < q_hi; ++q) {
+                    const int b = q * S + st;
+                    if (C::kPerGroupIssuer) tc3::mbar_wait_sleep(&a_ready[b], (ph >> b) & 1u);
+                    else tc::mbar_wait(&a_ready[b], (ph >> b) & 1u);
+                    ph ^= 1u << b;
+                    __syncwarp();
+                    tc::fence_after();
+                    tc3::issue_config(tmem_base + C::d_col(q, st), tmem_base + C::a_col(q, st),
+                                      bq0, bq1, bq2, &d_ready[b]);
+                }
+                st = st + 1 == S ? 0 : st + 1;
+            }
+        }
+    } else {
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        uint32_t ta[S], td[S], ph[S];
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) {
+            ta[s2] = tmem_base + lane_off + C::a_col(g, s2);
+            td[s2] = tmem_base + lane_off + C::d_col(g, s2);
+            ph[s2] = 0;
+            tc2::tmem_st_zero4(ta[s2] + 20);      // never-written tail (columns 20-23)
+        }
+        tc2::tmem_st_wait();
+        uint64_t *ar = &a_ready[g * S], *dr = &d_ready[g * S];
+
+        // head weights from shared memory (the fp32 copy staged above), so
+        // ptxas keeps them in registers instead of re-loading the constant
+        // bank every config
+        float2 wo2[9];
+#pragma unroll
+        for (int o = 0; o < 9; ++o) wo2[o] = make_float2(wo_s[2 * o], wo_s[2 * o + 1]);
+        const float bo = wo_s[HD];
+        int clamps[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) clamps[l] = 0;
+        const int member = t & 1;
+
+        for (int64_t blk = (int64_t)blockIdx.x * G + g; blk < nblocks; blk += total_groups) {
+            const int64_t pl = blk * tc::kPairsPerBlock + (t >> 1);
+            const bool live = pl < a.P;
+            int i = 0, j = 1;
+            if (live) pair_of(a.p_begin + pl, a.n, i, j);
+            const int self = member ? j : i, other = member ? i : j;
+            float2 p2[9];
+            {
+                float p[HD], tmp[HD];
+                load_row20(a.t.app_a32 + (size_t)self * ROW32, p);
+                load_row20(a.t.app_b32 + (size_t)other * ROW32, tmp);
+#pragma unroll
+                for (int w = 0; w < 9; ++w)
+                    p2[w] = make_float2(p[2 * w] + tmp[2 * w], p[2 * w + 1] + tmp[2 * w + 1]);
+            }
+            const float T_self = (float)a.base_time[self];
+            const uint32_t krow = tc::smem_u32(k12 + member * ROW32);   // + c * 2 * ROW32 * 4
+
+            float best[L], second[L];
+            int idx[L], bcl[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; bcl[l] = 0; }
+
+            // epilogue of config c from stage s (s compile-time after unrolling)
+            auto epilogue = [&](int c, int s) {
+                tc::mbar_wait(&dr[s], ph[s]);
+                ph[s] ^= 1u;
+                __syncwarp();
+                tc::fence_after();
+                const float y = tc3::head_from_tmem(td[s], wo2, bo);
+                const int cl = y < 0.5f;
+                const float tm = fmaxf(y, 0.5f) * T_self;
+                const float tt = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
+                const uint32_t m = L == 1 ? 1u : masks[c];
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    if (L == 1 || ((m >> l) & 1u)) {
+                        bcl[l] += cl;
+                        if (tt < best[l]) { second[l] = best[l]; best[l] = tt; idx[l] = c; }
+                        else second[l] = fminf(second[l], tt);
+                    }
+                }
+            };
+            auto build = [&](int c, int s) {
+                tc3::build_row(p2, krow + (uint32_t)c * (2 * ROW32 * 4), ta[s]);
+                if (C::kElected) {
+                    __syncwarp();
+                    if (lane == 0) tc2::mbar_arrive(&ar[s]);
+                } else {
+                    tc3::mbar_arrive_all(&ar[s]);
+                }
+                asm volatile("" ::: "memory");   // keep build / epilogue phases apart
+            };
+
+            // software pipeline, stage of config c = c % S:
+            //   build(0 .. S-2); [build(c), epilogue(c-S+1)] for c >= S-1; drain
+#pragma unroll
+            for (int u = 0; u < S - 1; ++u)
+                if (u < n_cfg) build(u, u);
+            int c = S - 1;                               // c % S == S - 1 throughout
+            for (; c + S <= n_cfg; c += S) {
+#pragma unroll
+                for (int u = 0; u < S; ++u) {
+                    build(c + u, (S - 1 + u) % S);
+                    epilogue(c + u - (S - 1), u % S);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2 * S - 1; ++u) {
+                const int cc = c + u, x = cc - (S - 1);
+                if (cc < n_cfg) build(cc, (S - 1 + u) % S);
+                if (x >= 0 && x < n_cfg) epilogue(x, u % S);
+            }
+#pragma unroll
+            for (int l = 0; l < L; ++l) clamps[l] += live ? bcl[l] : 0;
+
+            // ---- per (pair, budget): queue it, or re-evaluate the winner in fp64 ----
+#pragma unroll 1
+            for (int l = 0; l < L; ++l) {
+                const bool ambiguous = screen_ambiguous(a, best[l], second[l]);
+                const double tm64 = ambiguous ? 0.0
+                    : member_time64_lean(a.t, *net64, a.base_time, self, other, idx[l], member);
+                const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
+                if (live && member == 0) {
+                    if (ambiguous) push_ambiguous(a, l, pl);
+                    else write_winner(a, l, pl, idx[l], co, best[l]);
+                }
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            const int tot = __reduce_add_sync(0xffffffffu, clamps[l]);
+            if (lane == 0 && tot) atomicAdd(a.clamps + l, (unsigned long long)tot);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+inline size_t tc3_smem_bytes(int n_grid) {
+    size_t b = (size_t)tc2::kBBytes;
+    b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
+    b = (b + 7) & ~(size_t)7;
+    b += 2 * 16 * sizeof(uint64_t) + 16 + sizeof(Head64P) + 20 * sizeof(float);
+    return b;
+}

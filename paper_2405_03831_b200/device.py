@@ -118,8 +118,13 @@ class SweepPlan:
         self.n, self.grid, self.rel_eps = n, grid, float(rel_eps)
         kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT,
                  "tcgen05_smem": nat.KERNEL_TCGEN05_SMEM_A,
-                 # (compute groups, pipeline stages) variants of the TMEM-A screen
-                 "tcgen05_g4s2": 0x142, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
+                 # (compute groups, pipeline stages) variants of the v3 TMEM-A screen
+                 "tcgen05_v3": 0x142, "tcgen05_g4s2": 0x142,
+                 # (groups, stages) variants of the v4 screen (tc3_sweep.cuh)
+                 "tcgen05_v4_g3s3": 0x333, "tcgen05_v4_g4s2": 0x342,
+                 # + flags: 0x1000 elected a_ready arrive, 0x2000 per-group issuer warps
+                 **{f"tcgen05_v4_g{g}s{s}_f{v}": 0x300 | (g << 4) | s | (v << 12)
+                    for g, s in ((3, 3), (4, 2)) for v in range(4)}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         self.kernel, self.kernel_kind = kernel, kinds[kernel]

@@ -20,7 +20,7 @@ def _check(res, ref, L):
         assert np.array_equal(res.weight[l], ref["weight"][l])
 
 
-@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_smem", "simt", "tcgen05_g4s2",
+@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_v3", "tcgen05_smem", "simt",
                                     "tcgen05_g2s4"])
 @pytest.mark.parametrize("n,seed,budgets", [
     (20, 0, (400.0,)), (2, 1, (400.0,)), (67, 2, (350.0,)), (131, 3, (400.0, 350.0)),
@@ -35,7 +35,7 @@ def test_screen_kernels_match_oracle(weights, kernel, n, seed, budgets):
     assert res.screen_error < 1e-5, res.screen_error
 
 
-@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_smem", "simt"])
+@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_v3", "tcgen05_smem", "simt"])
 def test_five_budgets_and_fine_grid_shards(weights, kernel):
     levels = (300, 325, 350, 375, 400)
     spaces = [core.ConfigSpace(p_total=p, cap_sum_levels=levels) for p in (300.0, 325.0, 350.0, 375.0, 400.0)]
