@@ -393,7 +393,8 @@ def main():
     ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "tcgen05_v3", "tcgen05_smem", "simt", "tcgen05_g4s2",
                              "tcgen05_g3s3", "tcgen05_g2s4", "tcgen05_v4_g3s3",
                              "tcgen05_v4_g4s2"] + [f"tcgen05_v4_g{g}s{s}_f{v}" for g, s in
-                                                   ((3, 3), (4, 2)) for v in range(4)],
+                                                   ((3, 3), (4, 2)) for v in range(4)]
+                    + ["tcgen05_v4_g4s2_f5", "tcgen05_v4_g3s3_f5"],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -144,6 +144,13 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
 int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
             const double *d_base_time, cs_solo_out out, void *stream);
 
+/* cs_build_tables + cs_solo in ONE launch (each app's warp also evaluates its
+ * exclusive splits; falls back to two launches when a grid stacks more than 32
+ * solo splits).  Results identical to the two calls. */
+int cs_prepare(const cs_network *net, const double *d_features, const double *d_base_time,
+               int32_t n_apps, const cs_grid *d_grid, const cs_tables *tables, cs_solo_out out,
+               void *stream);
+
 /* The pair sweep is three stream-ordered steps (cs_solo may run concurrently
  * with the first two; only cs_pair_decide reads the solo results):
  *
@@ -180,6 +187,31 @@ int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_
 int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32_t *d_solo_clamps,
                    int32_t n_apps, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
                    unsigned long long *d_clamps, double *d_w, void *stream);
+
+/* The pair sweep in TWO launches (tcgen05 v4 screen only: CS_KERNEL_AUTO /
+ * CS_KERNEL_TCGEN05 or a 0xV3GS variant): the screen decides every
+ * unambiguous (pair, budget) itself -- co-run vs time-share against
+ * d_solo_time (cs_prepare / cs_solo, stream-ordered before) and the scatter
+ * into d_w (L x N x N, zeroed once by the caller; NULL to skip) -- and k_resolve
+ * does the same for the queued ones after their exact fp64 re-scan.  Same
+ * results and counters as cs_pair_screen + cs_resolve + cs_pair_decide. */
+int cs_pair_sweep_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                        const double *d_base_time, const double *d_solo_time,
+                        const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                        double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                        unsigned long long *d_clamps, double *d_w, int kernel_kind, void *stream);
+/* Its two launches separately (cs_pair_sweep_fused = screen_fused + resolve_fused). */
+int cs_pair_screen_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                         const double *d_base_time, const double *d_solo_time,
+                         const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                         double rel_eps, cs_pair_out out, int64_t *d_queue,
+                         uint32_t *d_queue_count, unsigned long long *d_clamps, double *d_w,
+                         int kernel_kind, void *stream);
+int cs_resolve_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                     cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, double *d_w, void *stream);
 
 int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                   const double *d_base_time, const double *d_solo_time,

@@ -79,6 +79,9 @@ SWEEP_SYMBOLS = {
     "cs_build_tables": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_int32,
                                        ctypes.POINTER(CsGrid), ctypes.POINTER(CsTables),
                                        ctypes.c_void_p]),
+    "cs_prepare": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_int32, ctypes.POINTER(CsGrid), ctypes.POINTER(CsTables),
+                                  CsSoloOut, ctypes.c_void_p]),
     "cs_solo": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
                                ctypes.POINTER(CsGrid), ctypes.c_void_p, CsSoloOut, ctypes.c_void_p]),
     "cs_pair_sweep": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
@@ -97,6 +100,23 @@ SWEEP_SYMBOLS = {
                                       ctypes.c_int64, ctypes.c_double, CsPairOut, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.c_void_p]),
+    "cs_pair_sweep_fused": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                                           ctypes.POINTER(CsGrid), ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_double, CsPairOut,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "cs_pair_screen_fused": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                                            ctypes.POINTER(CsGrid), ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.c_double, CsPairOut,
+                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "cs_resolve_fused": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                                        ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                        CsPairOut, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_resolve": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
                                   ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_int64, CsPairOut, ctypes.c_void_p, ctypes.c_void_p,

@@ -243,6 +243,11 @@ struct SweepArgs {
     uint32_t *qcount;
     unsigned long long *clamps;
     uint32_t *trace;         // debug builds (CS_TC_TRACE): per-thread progress, host-mapped
+    // fused tail (k_sweep_tc3 via cs_pair_sweep_fused): ambiguous pairs are
+    // re-scanned in fp64 inside the kernel, and every (pair, budget) is
+    // decided against solo_time and scattered into W (L x N x N, optional)
+    int fused;
+    double *W;
 };
 
 __device__ __forceinline__ bool screen_ambiguous(const SweepArgs &a, float best, float second) {
@@ -264,6 +269,28 @@ __device__ __forceinline__ void write_winner(const SweepArgs &a, int l, int64_t 
     a.out.corun_grid_index[o] = idx;
     a.out.corun_time[o] = co;
     atomicMax(a.qcount + 1, __float_as_uint((float)(fabs(co - (double)best) / co)));
+}
+
+// co-run vs time-share for one (pair, budget) (hwopt.py:77-87) with the solo
+// pair sum (0.0 + t_i) + t_j (estimator.py:168-178); writes the flag and the
+// winning time, scatters it into W, and returns the solo-split floor clamps the
+// reference counts for this pair (its two solorun_time calls)
+template <class Args>
+__device__ __forceinline__ int decide_write(const Args &a, int l, int64_t pl, int i, int j,
+                                            int idx, double co) {
+    const int64_t o = (int64_t)l * a.P + pl;
+    const double *st = a.solo_time + (size_t)l * a.n;
+    const double solo = (0.0 + st[i]) + st[j];
+    const bool chosen = idx >= 0 && co <= solo;
+    const double w = chosen ? co : solo;
+    a.out.corun_chosen[o] = chosen;
+    a.out.weight[o] = w;
+    if (a.W) {
+        double *Wl = a.W + (size_t)l * a.n * a.n;
+        Wl[(size_t)i * a.n + j] = w;
+        Wl[(size_t)j * a.n + i] = w;
+    }
+    return a.solo_clamps ? a.solo_clamps[(size_t)l * a.n + i] + a.solo_clamps[(size_t)l * a.n + j] : 0;
 }
 
 __device__ __forceinline__ float head32(const Net32P &net, const float (&z)[HD]) {
@@ -298,16 +325,66 @@ __device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
-// One thread per (row, hidden unit): rows are the N apps (A and B partials),
-// then the G configs (K1 and K2, b1 folded), then the S solo splits (KS).
-// The first W2_TILE_ELEMS threads also write the fp16 B operands.
+// The network is staged in shared memory once per block: the kernel parameter
+// bank serializes lane-divergent reads (lane h reading w1[h][k] is 18
+// different addresses), shared memory serves them in one wavefront; w1 is
+// also kept transposed (w1t[k][h]) so lane h's reads are consecutive.
+struct TablesSmem {
+    Net64P net;
+    double w1t[IN][HD];
+    Head64P head;
+};
+
+// Best split of budget l for this warp's app from the splits evaluated by
+// lanes [s0, s1) (value `tt`, INFINITY outside): first index wins ties
+// (estimator.py:175), clamps counted over the budget's splits.
+__device__ __forceinline__ void solo_reduce(double tt, int clamp, int lane, int s0, int s1,
+                                            int64_t w, cs_solo_out out) {
+    const bool in = lane >= s0 && lane < s1;
+    double best = in ? tt : INFINITY;
+    int arg = in ? lane - s0 : INT_MAX;
+    for (int off = 16; off; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, arg, off);
+        if (ob < best || (ob == best && oi < arg)) { best = ob; arg = oi; }
+    }
+    const int cl = __reduce_add_sync(0xffffffffu, in ? clamp : 0);
+    if (lane == 0) {
+        out.solo_time[w] = arg == INT_MAX ? nan("") : best;
+        out.solo_split[w] = arg == INT_MAX ? -1 : arg;
+        if (out.solo_clamps) out.solo_clamps[w] = cl;
+    }
+}
+
 // One warp per row -- the N apps (A and B partials), then the G configs (K1,
 // K2, b1 folded), then the S solo splits (KS) -- with lane h < 18 producing
 // hidden unit h; for app rows lane k first normalizes counter k (the fp64
-// divisions happen once per app).  Threads below W2_TILE_ELEMS also write the
-// fp16 B operands of the tensor-core screens.
-__global__ void k_tables(const __grid_constant__ Net64P net, const double *__restrict__ feats,
-                         int n, const GridP g, const cs_tables t) {
+// divisions happen once per app).  With `do_solo` (S <= 32) an app's warp
+// then also evaluates its S exclusive splits (lane s = split s, the exact fp64
+// head of k_solo) and reduces them per budget, so the solo step needs no
+// launch of its own.  Threads below W2_TILE_ELEMS also write the fp16 B
+// operands of the tensor-core screens.
+__global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P net_p,
+                                                const double *__restrict__ feats, int n,
+                                                const GridP g, const cs_tables t,
+                                                const double *__restrict__ base_time,
+                                                cs_solo_out solo, int do_solo) {
+    __shared__ TablesSmem sm;
+    {
+        const double *src = reinterpret_cast<const double *>(&net_p);
+        double *dst = reinterpret_cast<double *>(&sm.net);
+        for (int i = threadIdx.x; i < (int)(sizeof(Net64P) / 8); i += blockDim.x) dst[i] = src[i];
+        for (int i = threadIdx.x; i < HD * IN; i += blockDim.x) {
+            const int h = i / IN, k = i - h * IN;
+            sm.w1t[k][h] = net_p.w1[i];
+        }
+    }
+    __syncthreads();
+    // Head64P = {w2, b2, wo, bo}: the same 361 doubles as Net64P's w2 .. bo
+    for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / 8); i += blockDim.x)
+        reinterpret_cast<double *>(&sm.head)[i] = reinterpret_cast<const double *>(sm.net.w2)[i];
+    __syncthreads();
+    const Net64P &net = sm.net;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid < W2_TILE_ELEMS / 2) write_b_tile(net, t.w2_tile, (int)tid);
     else if (tid < W2_TILE_ELEMS) write_b_slices(net, t.w2_tile + W2_TILE_ELEMS / 2, (int)tid - W2_TILE_ELEMS / 2);
@@ -322,8 +399,8 @@ __global__ void k_tables(const __grid_constant__ Net64P net, const double *__res
             double sa = 0.0, sb = 0.0;
 #pragma unroll
             for (int k = 0; k < NF; ++k) {
-                sa = fma(__shfl_sync(0xffffffffu, x1, k), net.w1[h * IN + 4 + k], sa);
-                sb = fma(__shfl_sync(0xffffffffu, x2, k), net.w1[h * IN + 4 + NF + k], sb);
+                sa = fma(__shfl_sync(0xffffffffu, x1, k), sm.w1t[4 + k][h], sa);
+                sb = fma(__shfl_sync(0xffffffffu, x2, k), sm.w1t[4 + NF + k][h], sb);
             }
             if (lane < HD) {
                 t.app_a64[r * HD + h] = sa;
@@ -334,13 +411,33 @@ __global__ void k_tables(const __grid_constant__ Net64P net, const double *__res
                 t.app_a32[r * ROW32 + lane] = 0.f;
                 t.app_b32[r * ROW32 + lane] = 0.f;
             }
+            if (do_solo) {
+                // lane s: split s (all budgets' splits stacked, S <= 32); its
+                // KS row exactly as the solo-row branch below computes it
+                const int s = lane < g.S ? lane : 0;
+                double z[HD];
+#pragma unroll
+                for (int hh = 0; hh < HD; ++hh) {
+                    double ks = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) ks = fma(g.solo_knob[s * 4 + k], sm.w1t[k][hh], ks);
+                    ks = ks + net.b1[hh];
+                    z[hh] = __shfl_sync(0xffffffffu, sa, hh) + ks;
+                }
+                double y = head64_lean(sm.head, z);
+                int clamp = 0;
+                if (y < FLOOR) { clamp = 1; y = FLOOR; }
+                const double tt = y * base_time[r];
+                for (int l = 0; l < g.L; ++l)
+                    solo_reduce(tt, clamp, lane, g.solo_off[l], g.solo_off[l + 1], (int64_t)l * n + r, solo);
+            }
         } else if (r < (int64_t)n + g.G) {
             const int64_t c = r - n;
             double s1 = 0.0, s2 = 0.0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                s1 = fma(g.knob1[c * 4 + k], net.w1[h * IN + k], s1);
-                s2 = fma(g.knob2[c * 4 + k], net.w1[h * IN + k], s2);
+                s1 = fma(g.knob1[c * 4 + k], sm.w1t[k][h], s1);
+                s2 = fma(g.knob2[c * 4 + k], sm.w1t[k][h], s2);
             }
             s1 = s1 + net.b1[h];
             s2 = s2 + net.b1[h];
@@ -357,7 +454,7 @@ __global__ void k_tables(const __grid_constant__ Net64P net, const double *__res
             const int64_t c = r - n - g.G;
             double s1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) s1 = fma(g.solo_knob[c * 4 + k], net.w1[h * IN + k], s1);
+            for (int k = 0; k < 4; ++k) s1 = fma(g.solo_knob[c * 4 + k], sm.w1t[k][h], s1);
             if (lane < HD) t.solo64[c * HD + h] = s1 + net.b1[h];
         }
     }
@@ -490,6 +587,11 @@ struct ResolveArgs {
     cs_pair_out out;
     const int64_t *queue;
     const uint32_t *qcount;
+    // fused (cs_pair_sweep_fused): also decide + scatter each resolved entry
+    int fused;
+    const int32_t *solo_clamps;
+    unsigned long long *clamps;
+    double *W;
 };
 
 __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
@@ -528,6 +630,11 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
             const int64_t o = (int64_t)l * a.P + pl;
             a.out.corun_grid_index[o] = arg == INT_MAX ? -1 : arg;
             a.out.corun_time[o] = arg == INT_MAX ? INFINITY : best;
+            if (a.fused) {
+                const int cl = decide_write(a, l, pl, i, j, arg == INT_MAX ? -1 : arg,
+                                            arg == INT_MAX ? INFINITY : best);
+                if (cl) atomicAdd(a.clamps + l, (unsigned long long)cl);
+            }
         }
         __syncthreads();
     }
@@ -716,6 +823,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
             return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
         CS_TC3(3, 3, 0) CS_TC3(3, 3, 1) CS_TC3(3, 3, 2) CS_TC3(3, 3, 3)
         CS_TC3(4, 2, 0) CS_TC3(4, 2, 1) CS_TC3(4, 2, 2) CS_TC3(4, 2, 3)
+        CS_TC3(4, 2, 5) CS_TC3(3, 3, 5)
 #undef CS_TC3
         return CS_ERR_ARG;
     }
@@ -793,8 +901,10 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
     return CS_OK;
 }
 
-int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
-                    const cs_grid *d_grid, const cs_tables *tables, void *stream) {
+namespace {
+int launch_tables(const cs_network *net, const double *d_features, int32_t n_apps,
+                  const cs_grid *d_grid, const cs_tables *tables, const double *d_base_time,
+                  cs_solo_out solo, int do_solo, void *stream) {
     Net64P np;
     if (!net64_from(net, &np) || !tables || n_apps < 2 || !d_features) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
@@ -805,8 +915,29 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
     int64_t threads = items > W2_TILE_ELEMS ? items : W2_TILE_ELEMS;
     int blocks = (int)((threads + 127) / 128);
     if (blocks > sm_count() * 16) blocks = sm_count() * 16;
-    k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables);
+    k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables,
+                                                        d_base_time, solo, do_solo);
     return check_launch();
+}
+}  // namespace
+
+int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
+                    const cs_grid *d_grid, const cs_tables *tables, void *stream) {
+    return launch_tables(net, d_features, n_apps, d_grid, tables, nullptr, cs_solo_out{}, 0, stream);
+}
+
+int cs_prepare(const cs_network *net, const double *d_features, const double *d_base_time,
+               int32_t n_apps, const cs_grid *d_grid, const cs_tables *tables, cs_solo_out out,
+               void *stream) {
+    int rc = check_grid(d_grid);
+    if (rc) return rc;
+    if (!d_base_time || !out.solo_time || !out.solo_split) return CS_ERR_ARG;
+    const int S = d_grid->solo_offsets[d_grid->n_budgets];
+    if (S <= 32)   // one warp per app evaluates all its splits
+        return launch_tables(net, d_features, n_apps, d_grid, tables, d_base_time, out, 1, stream);
+    rc = launch_tables(net, d_features, n_apps, d_grid, tables, nullptr, cs_solo_out{}, 0, stream);
+    if (rc) return rc;
+    return cs_solo(net, tables, d_grid, d_base_time, out, stream);
 }
 
 int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
@@ -823,10 +954,75 @@ int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_gri
     return check_launch();
 }
 
+namespace {
+int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, int kernel_kind, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, double *d_w, int fused, void *stream);
+}
+
 int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                    const double *d_base_time, int64_t pair_begin, int64_t pair_end,
                    double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                    unsigned long long *d_clamps, int kernel_kind, void *stream) {
+    return pair_screen_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
+                            d_queue, d_queue_count, d_clamps, kernel_kind, nullptr, nullptr,
+                            nullptr, 0, stream);
+}
+
+namespace {
+int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                 const double *d_base_time, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
+                 const int64_t *d_queue, const uint32_t *d_queue_count, const double *d_solo_time,
+                 const int32_t *d_solo_clamps, unsigned long long *d_clamps, double *d_w,
+                 int fused, void *stream);
+}
+
+int cs_pair_screen_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                         const double *d_base_time, const double *d_solo_time,
+                         const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                         double rel_eps, cs_pair_out out, int64_t *d_queue,
+                         uint32_t *d_queue_count, unsigned long long *d_clamps, double *d_w,
+                         int kernel_kind, void *stream) {
+    if (!d_solo_time || !out.corun_chosen || !out.weight || !d_queue) return CS_ERR_ARG;
+    if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
+    if (kernel_kind != CS_KERNEL_TCGEN05 && (kernel_kind & 0xF00) != 0x300) return CS_ERR_ARG;
+    return pair_screen_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
+                            d_queue, d_queue_count, d_clamps, kernel_kind, d_solo_time,
+                            d_solo_clamps, d_w, 1, stream);
+}
+
+int cs_resolve_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                     cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, double *d_w, void *stream) {
+    if (!d_solo_time || !out.corun_chosen || !out.weight || !d_clamps) return CS_ERR_ARG;
+    return resolve_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
+                        d_queue_count, d_solo_time, d_solo_clamps, d_clamps, d_w, 1, stream);
+}
+
+int cs_pair_sweep_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                        const double *d_base_time, const double *d_solo_time,
+                        const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
+                        double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                        unsigned long long *d_clamps, double *d_w, int kernel_kind, void *stream) {
+    int rc = cs_pair_screen_fused(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
+                                  pair_begin, pair_end, rel_eps, out, d_queue, d_queue_count,
+                                  d_clamps, d_w, kernel_kind, stream);
+    if (rc) return rc;
+    return cs_resolve_fused(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
+                            pair_begin, pair_end, out, d_queue, d_queue_count, d_clamps, d_w,
+                            stream);
+}
+
+namespace {
+int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                     const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     unsigned long long *d_clamps, int kernel_kind, const double *d_solo_time,
+                     const int32_t *d_solo_clamps, double *d_w, int fused, void *stream) {
     Net64P n64;
     if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
@@ -859,6 +1055,10 @@ int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid
     a.qcount = d_queue_count;
     a.clamps = d_clamps;
     a.trace = nullptr;
+    a.fused = fused;
+    a.W = d_w;
+    a.solo_time = d_solo_time;
+    a.solo_clamps = d_solo_clamps;
 #ifdef CS_TC_TRACE
     a.trace = (uint32_t *)getenv_ptr("CS_TC_TRACE_PTR");
 #endif
@@ -896,6 +1096,7 @@ int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid
     if (lrc) return lrc;
     return check_launch();
 }
+}  // namespace
 
 int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32_t *d_solo_clamps,
                    int32_t n_apps, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
@@ -950,10 +1151,12 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
                           pair_end, out, d_clamps, nullptr, stream);
 }
 
-int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
-               const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
-               void *stream) {
+namespace {
+int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+                 const double *d_base_time, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
+                 const int64_t *d_queue, const uint32_t *d_queue_count, const double *d_solo_time,
+                 const int32_t *d_solo_clamps, unsigned long long *d_clamps, double *d_w,
+                 int fused, void *stream) {
     Net64P n64;
     if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
@@ -970,9 +1173,24 @@ int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_
     a.out = out;
     a.queue = d_queue;
     a.qcount = d_queue_count;
-    // the queue length lives on the device: launch a resident grid, block-stride
-    k_resolve<<<sm_count() * 8, 128, 0, (cudaStream_t)stream>>>(a, head64_from(n64));
+    a.fused = fused;
+    a.solo_time = d_solo_time;
+    a.solo_clamps = d_solo_clamps;
+    a.clamps = d_clamps;
+    a.W = d_w;
+    // the queue length lives on the device: one resident wave of blocks that
+    // stride over it (an oversized grid costs a launch wave per 148 x 16 blocks)
+    k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a, head64_from(n64));
     return check_launch();
+}
+}  // namespace
+
+int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
+               const double *d_base_time, int64_t pair_begin, int64_t pair_end,
+               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+               void *stream) {
+    return resolve_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
+                        d_queue_count, nullptr, nullptr, nullptr, nullptr, 0, stream);
 }
 
 int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,
@@ -1092,21 +1310,17 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     dg.solo_knob = (const double *)(ws + L.solo_knob);
     cs_tables t;
     CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
-    CS_RC(cs_build_tables(net, (const double *)(ws + L.feats), n_apps, &dg, &t, stream));
     cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
                    (int32_t *)(ws + L.solo_clamps)};
-    CS_RC(cs_solo(net, &t, &dg, (const double *)(ws + L.bt), so, stream));
+    CS_RC(cs_prepare(net, (const double *)(ws + L.feats), (const double *)(ws + L.bt), n_apps, &dg,
+                     &t, so, stream));
     cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
-    CS_RC(cs_pair_screen(net, &t, &dg, (const double *)(ws + L.bt), 0, P, rel_eps, po,
-                         (int64_t *)(ws + L.queue), (uint32_t *)(ws + L.qcount),
-                         (unsigned long long *)(ws + L.clamps), CS_KERNEL_AUTO, stream));
-    CS_RC(cs_resolve(net, &t, &dg, (const double *)(ws + L.bt), 0, P, po,
-                     (const int64_t *)(ws + L.queue), (const uint32_t *)(ws + L.qcount), stream));
     if (h_weights) CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n * nb, st));
-    CS_RC(cs_pair_decide(&dg, so.solo_time, so.solo_clamps, n_apps, 0, P, po,
-                         (unsigned long long *)(ws + L.clamps),
-                         h_weights ? (double *)(ws + L.W) : nullptr, stream));
+    CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
+                              so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue),
+                              (uint32_t *)(ws + L.qcount), (unsigned long long *)(ws + L.clamps),
+                              h_weights ? (double *)(ws + L.W) : nullptr, CS_KERNEL_AUTO, stream));
     if (h_weights)
         CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
                                cudaMemcpyDeviceToHost, st));

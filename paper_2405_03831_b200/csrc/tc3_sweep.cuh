@@ -23,12 +23,15 @@ namespace tc3 {
 
 // V bit 0: one elected arrive per warp on a_ready (count 4) instead of all
 //           128 threads arriving;
-// V bit 1: one MMA-issuer warp per group instead of one shared issuer.
+// V bit 1: one MMA-issuer warp per group instead of one shared issuer;
+// V bit 2: no issuer warps -- the group's own compute warps take turns (warp
+//          c % 4 issues config c), so 4 warps per scheduler get 128 registers.
 template <int G, int S, int V = 0>
 struct Cfg {
     static constexpr bool kElected = (V & 1) != 0;
     static constexpr bool kPerGroupIssuer = (V & 2) != 0;
-    static constexpr int kIssuers = kPerGroupIssuer ? G : 1;
+    static constexpr bool kComputeIssue = (V & 4) != 0;
+    static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
     static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
     __device__ static constexpr uint32_t d_col(int g, int s) { return (uint32_t)((g * S + s) * 32); }
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     const int64_t total_groups = (int64_t)gridDim.x * G;
     const int n_cfg = a.g.G;
 
-    if (g >= G) {
+    if (!C::kComputeIssue && g >= G) {
         // ===== one MMA-issuer warp serves the G groups in lockstep =====
         // Every active group of a round sweeps the same configs in the same
         // order, so the issuer visits (config k, group q) round-robin.
@@ -238,12 +241,17 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
         }
     } else {
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        uint32_t ta[S], td[S], ph[S];
+        uint32_t ta[S], td[S], ph[S], aph[S];
+        const uint32_t b_addr = tc::smem_u32(b_tile);
+        const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
+                       bq2 = tc2::slice_desc(b_addr + 2048);
+        const int wg = warp & 3;                  // warp within the group
 #pragma unroll
         for (int s2 = 0; s2 < S; ++s2) {
             ta[s2] = tmem_base + lane_off + C::a_col(g, s2);
             td[s2] = tmem_base + lane_off + C::d_col(g, s2);
             ph[s2] = 0;
+            aph[s2] = 0;
             tc2::tmem_st_zero4(ta[s2] + 20);      // never-written tail (columns 20-23)
         }
         tc2::tmem_st_wait();
@@ -312,6 +320,16 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 } else {
                     tc3::mbar_arrive_all(&ar[s]);
                 }
+                if (C::kComputeIssue) {
+                    if ((c & 3) == wg) {          // this warp's turn to issue config c
+                        tc::mbar_wait(&ar[s], aph[s]);
+                        __syncwarp();
+                        tc::fence_after();
+                        tc3::issue_config(tmem_base + C::d_col(g, s), tmem_base + C::a_col(g, s),
+                                          bq0, bq1, bq2, &dr[s]);
+                    }
+                    aph[s] ^= 1u;
+                }
                 asm volatile("" ::: "memory");   // keep build / epilogue phases apart
             };
 
@@ -337,7 +355,8 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
 #pragma unroll
             for (int l = 0; l < L; ++l) clamps[l] += live ? bcl[l] : 0;
 
-            // ---- per (pair, budget): queue it, or re-evaluate the winner in fp64 ----
+            // ---- per (pair, budget): queue it (k_resolve), or re-evaluate the
+            //      winner in fp64 and, fused, decide + scatter it right here ----
 #pragma unroll 1
             for (int l = 0; l < L; ++l) {
                 const bool ambiguous = screen_ambiguous(a, best[l], second[l]);
@@ -345,8 +364,12 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     : member_time64_lean(a.t, *net64, a.base_time, self, other, idx[l], member);
                 const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
                 if (live && member == 0) {
-                    if (ambiguous) push_ambiguous(a, l, pl);
-                    else write_winner(a, l, pl, idx[l], co, best[l]);
+                    if (ambiguous) {
+                        push_ambiguous(a, l, pl);
+                    } else {
+                        write_winner(a, l, pl, idx[l], co, best[l]);
+                        if (a.fused) clamps[l] += decide_write(a, l, pl, i, j, idx[l], co);
+                    }
                 }
             }
         }

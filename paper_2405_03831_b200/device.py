@@ -124,7 +124,8 @@ class SweepPlan:
                  "tcgen05_v4_g3s3": 0x333, "tcgen05_v4_g4s2": 0x342,
                  # + flags: 0x1000 elected a_ready arrive, 0x2000 per-group issuer warps
                  **{f"tcgen05_v4_g{g}s{s}_f{v}": 0x300 | (g << 4) | s | (v << 12)
-                    for g, s in ((3, 3), (4, 2)) for v in range(4)}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
+                    for g, s, v in [(3, 3, v) for v in range(4)] + [(4, 2, v) for v in range(4)]
+                    + [(4, 2, 5), (3, 3, 5)]}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
@@ -164,7 +165,11 @@ class SweepPlan:
             ctypes.cast(_dptr(self.solo_split), nat.c_int32_p),
             ctypes.cast(_dptr(self.solo_clamps), nat.c_int32_p))
         self._side = torch.cuda.Stream(self.device)
-        self.launches_per_run = 6
+        # the v4 tcgen05 screen runs the fused pipeline: k_tables (+ solo
+        # splits) -> k_sweep_tc3 (+ decide/scatter) -> k_resolve (+ decide);
+        # the other screens keep tables | solo -> screen -> resolve -> decide
+        self.fused = kernel == "tcgen05" or kernel.startswith("tcgen05_v4")
+        self.launches_per_run = 3 if self.fused else 5
 
     # ------------------------------------------------------------------
     def launch(self, d_features: torch.Tensor, d_base_time: torch.Tensor,
@@ -187,17 +192,41 @@ class SweepPlan:
         self.counters.zero_()
         self.clamps.zero_()
         tref = ctypes.byref(self.tables)
+        cnt = _dptr(self.counters)
+        if self.fused:
+            nat.check(lib.cs_prepare(self.net.ref(), _dptr(d_features), _dptr(d_base_time), n,
+                                     self.dgrid.ref(), tref, self.solo_out, st), "cs_prepare")
+            if self.P == 0:
+                return
+            # the symmetric matrix is scattered in-kernel when this plan owns
+            # the whole graph (its diagonal stays zero from allocation)
+            w = _dptr(self.matrix) if (self.matrix is not None and self.P == n_pairs(n)) else None
+            if sweep_events is not None:
+                sweep_events[0].record(cur)
+            nat.check(lib.cs_pair_screen_fused(
+                self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time), _dptr(self.solo_time),
+                _dptr(self.solo_clamps), self.pair_begin, self.pair_end, self.rel_eps,
+                self.pair_out, _dptr(self.queue), cnt, _dptr(self.clamps), w, self.kernel_kind,
+                st), "cs_pair_screen_fused")
+            if sweep_events is not None:
+                sweep_events[1].record(cur)
+            nat.check(lib.cs_resolve_fused(
+                self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time), _dptr(self.solo_time),
+                _dptr(self.solo_clamps), self.pair_begin, self.pair_end, self.pair_out,
+                _dptr(self.queue), cnt, _dptr(self.clamps), w, st), "cs_resolve_fused")
+            if self.matrix is not None and w is None:
+                self.scatter(st)
+            return
         nat.check(lib.cs_build_tables(self.net.ref(), _dptr(d_features), n, self.dgrid.ref(),
                                       tref, st), "cs_build_tables")
         # solo splits run on a side stream, concurrently with the pair screen
-        # (the screen does not read them; cs_pair_finalize does)
+        # (the screen does not read them; cs_pair_decide does)
         self._side.wait_stream(cur)
         nat.check(lib.cs_solo(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
                               self.solo_out, self._side.cuda_stream), "cs_solo")
         if self.P == 0:
             cur.wait_stream(self._side)
             return
-        cnt = _dptr(self.counters)
         if sweep_events is not None:
             sweep_events[0].record(cur)
         nat.check(lib.cs_pair_screen(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
