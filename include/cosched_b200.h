@@ -113,6 +113,7 @@ typedef struct {
     float *knob1_32, *knob2_32;   /* G x 20, b1 folded */
     double *knob1_64, *knob2_64;  /* G x 18, b1 folded */
     double *solo64;               /* S x 18, b1 folded */
+    double *net_image;            /* the network in device memory (cs_tables_set_network) */
 } cs_tables;
 
 /* Per-pair outputs of one shard, budget-major: element [l * P + (p - pair_begin)]. */
@@ -137,6 +138,13 @@ const char *cs_error_string(int code);
 size_t cs_tables_bytes(int32_t n_apps, int32_t n_grid, int32_t n_solo);
 int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, int32_t n_solo,
                    cs_tables *out);
+/* Copy the network into the tables' device image.  Call once after binding
+ * (and whenever the weights change) BEFORE any kernel call that takes these
+ * tables: the kernels read the weights from device memory (coalesced) instead
+ * of the kernel parameter bank, whose lane-divergent reads serialize.  The
+ * copy is issued on `stream` from pageable host memory (the call returns once
+ * the host data is staged), so it must not be captured into a CUDA graph. */
+int cs_tables_set_network(const cs_network *net, const cs_tables *tables, void *stream);
 
 int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
                     const cs_grid *d_grid, const cs_tables *tables, void *stream);

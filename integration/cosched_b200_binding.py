@@ -87,7 +87,7 @@ def _knob(cp, gp, cc, gc):
             cc / core.CPU_CAP_MAX, gc / core.GPU_CAP_MAX)
 
 
-def build_graph_b200(inp, rel_eps: float = 1e-4):
+def build_graph_b200(inp, rel_eps: float = 1e-5):
     """scheduler.build_graph for a trained network, in one C call."""
     model = inp.model
     w = model.weights if isinstance(model, estimator.FnnSlowdownModel) else model

@@ -57,7 +57,8 @@ class CsTables(ctypes.Structure):
                 ("w2_tile", ctypes.c_void_p), ("app_a32", c_float_p), ("app_b32", c_float_p),
                 ("app_a64", c_double_p), ("app_b64", c_double_p),
                 ("knob1_32", c_float_p), ("knob2_32", c_float_p),
-                ("knob1_64", c_double_p), ("knob2_64", c_double_p), ("solo64", c_double_p)]
+                ("knob1_64", c_double_p), ("knob2_64", c_double_p), ("solo64", c_double_p),
+                ("net_image", c_double_p)]
 
 
 class CsPairOut(ctypes.Structure):
@@ -79,6 +80,8 @@ SWEEP_SYMBOLS = {
     "cs_build_tables": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_int32,
                                        ctypes.POINTER(CsGrid), ctypes.POINTER(CsTables),
                                        ctypes.c_void_p]),
+    "cs_tables_set_network": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
+                                             ctypes.c_void_p]),
     "cs_prepare": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_int32, ctypes.POINTER(CsGrid), ctypes.POINTER(CsTables),
                                   CsSoloOut, ctypes.c_void_p]),

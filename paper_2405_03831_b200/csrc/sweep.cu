@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstddef>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -181,11 +182,18 @@ __device__ __forceinline__ double head64_lean(const Head64P &net, const double (
 // Stage the fp64 head weights in shared memory: 324+ distinct fp64 constants
 // overflow the per-SM constant cache, while a shared-memory copy is read with
 // broadcast LDS (every lane of a warp reads the same address).
-__device__ __forceinline__ const Head64P &stage_head64(const Head64P &param, Head64P &sm) {
-    const double *src = reinterpret_cast<const double *>(&param);
+// The device network image (cs_tables_set_network): Net64P, then w1
+// transposed (w1t[k][h]); Head64P = {w2, b2, wo, bo} is a contiguous slice of
+// Net64P.
+constexpr int kImgHeadOff = (HD * IN + HD);                  // doubles before Net64P::w2
+constexpr int kImgW1tOff = (int)(sizeof(Net64P) / 8);
+constexpr int kImgDoubles = kImgW1tOff + IN * HD;
+
+__device__ __forceinline__ const Head64P &stage_head64(const double *__restrict__ img, Head64P &sm) {
+    const double *src = img + kImgHeadOff;
     double *dst = reinterpret_cast<double *>(&sm);
     for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / sizeof(double)); i += blockDim.x)
-        dst[i] = src[i];
+        dst[i] = __ldg(src + i);
     __syncthreads();
     return sm;
 }
@@ -364,25 +372,24 @@ __device__ __forceinline__ void solo_reduce(double tt, int clamp, int lane, int 
 // head of k_solo) and reduces them per budget, so the solo step needs no
 // launch of its own.  Threads below W2_TILE_ELEMS also write the fp16 B
 // operands of the tensor-core screens.
-__global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P net_p,
+__global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P net_unused,
                                                 const double *__restrict__ feats, int n,
                                                 const GridP g, const cs_tables t,
                                                 const double *__restrict__ base_time,
                                                 cs_solo_out solo, int do_solo) {
     __shared__ TablesSmem sm;
     {
-        const double *src = reinterpret_cast<const double *>(&net_p);
+        // coalesced copy of the device image (Net64P | w1t): the parameter
+        // bank would serialize these lane-divergent reads
+        const double *img = t.net_image;
         double *dst = reinterpret_cast<double *>(&sm.net);
-        for (int i = threadIdx.x; i < (int)(sizeof(Net64P) / 8); i += blockDim.x) dst[i] = src[i];
-        for (int i = threadIdx.x; i < HD * IN; i += blockDim.x) {
-            const int h = i / IN, k = i - h * IN;
-            sm.w1t[k][h] = net_p.w1[i];
-        }
+        for (int i = threadIdx.x; i < kImgW1tOff; i += blockDim.x) dst[i] = __ldg(img + i);
+        double *w1t = &sm.w1t[0][0];
+        for (int i = threadIdx.x; i < IN * HD; i += blockDim.x) w1t[i] = __ldg(img + kImgW1tOff + i);
+        double *hd = reinterpret_cast<double *>(&sm.head);
+        for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / 8); i += blockDim.x)
+            hd[i] = __ldg(img + kImgHeadOff + i);
     }
-    __syncthreads();
-    // Head64P = {w2, b2, wo, bo}: the same 361 doubles as Net64P's w2 .. bo
-    for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / 8); i += blockDim.x)
-        reinterpret_cast<double *>(&sm.head)[i] = reinterpret_cast<const double *>(sm.net.w2)[i];
     __syncthreads();
     const Net64P &net = sm.net;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
 __global__ void k_solo(const cs_tables t, const GridP g, const double *__restrict__ base_time,
                        int n, cs_solo_out out, const __grid_constant__ Head64P net_param) {
     __shared__ Head64P net_sm;
-    const Head64P &net = stage_head64(net_param, net_sm);
+    const Head64P &net = stage_head64(t.net_image, net_sm);
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= (int64_t)n * g.L) return;
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
                                                          const __grid_constant__ Net32P net,
                                                          const __grid_constant__ Head64P net_param) {
     __shared__ Head64P net_sm;
-    const Head64P &net64 = stage_head64(net_param, net_sm);
+    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int S = 1 << a.log2s;
     const int64_t pl = gt >> a.log2s;          // local pair index
@@ -601,7 +608,7 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
     __shared__ Head64P net_sm;
     __shared__ double red_v[4];
     __shared__ int red_i[4];
-    const Head64P &net64 = stage_head64(net_param, net_sm);
+    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
     const uint32_t count = *a.qcount;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t q = blockIdx.x; q < count; q += gridDim.x) {
@@ -878,6 +885,7 @@ size_t cs_tables_bytes(int32_t n_apps, int32_t n_grid, int32_t n_solo) {
     b += 2 * align256(sizeof(float) * (size_t)n_grid * ROW32);
     b += 2 * align256(sizeof(double) * (size_t)n_grid * HD);
     b += align256(sizeof(double) * (size_t)n_solo * HD);
+    b += align256(sizeof(double) * (size_t)kImgDoubles);
     return b;
 }
 
@@ -898,6 +906,24 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
     out->knob1_64 = (double *)take(sizeof(double) * (size_t)n_grid * HD);
     out->knob2_64 = (double *)take(sizeof(double) * (size_t)n_grid * HD);
     out->solo64 = (double *)take(sizeof(double) * (size_t)n_solo * HD);
+    out->net_image = (double *)take(sizeof(double) * (size_t)kImgDoubles);
+    return CS_OK;
+}
+
+int cs_tables_set_network(const cs_network *net, const cs_tables *tables, void *stream) {
+    Net64P np;
+    if (!net64_from(net, &np) || !tables || !tables->net_image) return CS_ERR_ARG;
+    static_assert(offsetof(Net64P, w2) == sizeof(double) * kImgHeadOff, "image layout");
+    double img[kImgDoubles];
+    memcpy(img, &np, sizeof(Net64P));
+    for (int h = 0; h < HD; ++h)
+        for (int k = 0; k < IN; ++k) img[kImgW1tOff + k * HD + h] = np.w1[h * IN + k];
+    // pageable source: returns once the bytes are staged, so `img` may go out of scope
+    if (cudaMemcpyAsync(tables->net_image, img, sizeof(img), cudaMemcpyHostToDevice,
+                        (cudaStream_t)stream) != cudaSuccess) {
+        cudaGetLastError();
+        return CS_ERR_CUDA;
+    }
     return CS_OK;
 }
 
@@ -1310,6 +1336,7 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     dg.solo_knob = (const double *)(ws + L.solo_knob);
     cs_tables t;
     CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
+    CS_RC(cs_tables_set_network(net, &t, stream));
     cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
                    (int32_t *)(ws + L.solo_clamps)};
     CS_RC(cs_prepare(net, (const double *)(ws + L.feats), (const double *)(ws + L.bt), n_apps, &dg,

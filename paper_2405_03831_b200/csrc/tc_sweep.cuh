@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     }
     for (int i = tid; i < a.g.G; i += tc::kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
     for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += tc::kThreads)
-        reinterpret_cast<double *>(net64)[i] = reinterpret_cast<const double *>(&net_param)[i];
+        reinterpret_cast<double *>(net64)[i] = __ldg(a.t.net_image + kImgHeadOff + i);
     if (tid == 0) {
         for (int i = 0; i < 2 * tc::kGroups; ++i) tc::mbar_init(&mbars[i], 1);
         tc::fence_mbar_init();

@@ -29,7 +29,7 @@ from .grid import KnobGrid
 # The measured fp32 screen error is ~3e-7 relative (SURVEY.md §7 hard part 1);
 # the kernel reports the largest gap it saw (SweepPlan.screen_error) and
 # SweepPlan.launch() callers can assert it stays far below this.
-DEFAULT_REL_EPS = 1e-4
+DEFAULT_REL_EPS = 1e-5
 
 
 def require_cuda(device=None) -> torch.device:
@@ -142,6 +142,9 @@ class SweepPlan:
             self.tables = nat.CsTables()
             nat.check(self.lib.cs_tables_bind(base, nbytes, n, G, S, ctypes.byref(self.tables)),
                       "cs_tables_bind")
+            # the network goes to device memory once per plan (never per launch)
+            nat.check(self.lib.cs_tables_set_network(self.net.ref(), ctypes.byref(self.tables),
+                                                     _stream_handle(dev)), "cs_tables_set_network")
             P = max(self.P, 1)
             self.corun_grid_index = torch.empty((L, P), dtype=torch.int32, device=dev)
             self.corun_time = torch.empty((L, P), dtype=torch.float64, device=dev)

@@ -32,7 +32,7 @@ def test_screen_kernels_match_oracle(weights, kernel, n, seed, budgets):
     F, T = workload(n, seed)
     ref = oracle.sweep(weights, F, T, KnobGrid(spaces))
     _check(res, ref, len(spaces))
-    assert res.screen_error < 1e-5, res.screen_error
+    assert res.screen_error < 2.5e-6, res.screen_error
 
 
 @pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_v3", "tcgen05_smem", "simt"])

@@ -94,18 +94,30 @@ def full(rep: str, top: int = 40) -> str:
                     out.append(f"| {label} (`{key}`) | {row[i]} {u[i]} |")
             out.append("")
     src = list(csv.reader(io.StringIO(_ncu(rep, "--page", "source", "--csv", "--print-source", "sass"))))
-    if len(src) > 2:
-        h = src[1]
+    # one section per profiled kernel: a "Kernel Name" row, a header row, the body
+    sections, cur = [], None
+    for row in src:
+        if row and row[0] == "Kernel Name":
+            cur = {"name": row[1] if len(row) > 1 else "?", "rows": []}
+            sections.append(cur)
+        elif cur is not None:
+            cur["rows"].append(row)
+    for sec in sections:
+        if len(sec["rows"]) < 2:
+            continue
+        h = sec["rows"][0]
         ia, ie = h.index("Source"), h.index("Instructions Executed")
         iss = h.index("Warp Stall Sampling (All Samples)")
-        body = [r for r in src[2:] if len(r) == len(h)]
+        body = [r for r in sec["rows"][1:] if len(r) == len(h)]
         tot_e = sum(int(r[ie]) for r in body)
         tot_s = sum(int(r[iss]) for r in body) or 1
-        out.append(f"Source page: {tot_e} warp instructions executed, {tot_s} stall samples.\n")
+        out.append(f"Source page of `{_kernel_short(sec['name'])}`: {tot_e} warp instructions "
+                   f"executed, {tot_s} stall samples.\n")
         out.append(f"Top {top} SASS lines by stall samples:\n")
         out.append("| addr | executed | stall samples | SASS |\n|---|---|---|---|")
         for r in sorted(body, key=lambda r: -int(r[iss]))[:top]:
             out.append(f"| {r[0][-5:]} | {r[ie]} | {r[iss]} | `{r[ia].strip()}` |")
+        out.append("")
     return "\n".join(out)
 
 
