@@ -72,6 +72,17 @@ def load_weights():
     return fnn.load_weights(os.path.join(ROOT, "tests", "golden", "weights.json"))
 
 
+def measured_traffic(workload, kernel):
+    """DRAM bytes per launch of the sweep kernel from the committed ncu capture
+    (profiles/traffic.json, written by tools/ncu_summary.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            d = json.load(fh)
+        return d.get(f"{workload}/{kernel}")
+    except (OSError, ValueError):
+        return None
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -227,10 +238,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one rank per GPU; COSCHED_BENCH_SHARE_GPU lets a 1-GPU box run N ranks on
+    # cuda:0 (with the gloo backend) to exercise the sharded path
+    ndev = torch.cuda.device_count()
+    dev_index = local_rank % ndev
+    if world > ndev and not os.environ.get("COSCHED_BENCH_SHARE_GPU"):
+        raise SystemExit(f"{world} ranks but {ndev} GPU(s)")
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("COSCHED_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     weights = load_weights()
     n, spaces = spaces_for(args.workload)
@@ -243,6 +264,7 @@ def run_ours(args):
     d_f, d_b = to_device_inputs(F, T, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    graph_mode = "cuda-graph"
     ev_s = torch.cuda.Event(enable_timing=True, external=True)
     ev_e = torch.cuda.Event(enable_timing=True, external=True)
     if world == 1:
@@ -264,10 +286,32 @@ def run_ours(args):
         from paper_2405_03831_b200.dist import ShardedSweep
         sh = ShardedSweep(weights, grid, n, device=dev, kernel=args.kernel)
         plan = sh.plan
+        for _ in range(2):
+            sh.run(d_f, d_b)
+        torch.cuda.synchronize(dev)
+        ref_m = sh.matrix.clone()
 
         def step():
             sh.run(d_f, d_b, (ev_s, ev_e))
-        launches_per_step = 4 + grid.n_budgets
+        graph_mode = "eager"
+        if dist.get_backend() == "nccl" and not os.environ.get("COSCHED_NO_GRAPH"):
+            # the whole step -- shard sweep, NCCL all-gather, device scatter -- as
+            # one CUDA graph; kept only if its replay reproduces the eager matrix
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    sh.run(d_f, d_b, (ev_s, ev_e))
+                sh.matrix.zero_()
+                g.replay()
+                torch.cuda.synchronize(dev)
+                ok = torch.tensor([int(torch.equal(sh.matrix, ref_m))], device=dev)
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                if int(ok) == 1:
+                    step, graph_mode = g.replay, "cuda-graph (sweep + NCCL all-gather + scatter)"
+            except Exception as exc:   # capture unsupported here: stay eager
+                print(f"rank {rank}: graph capture failed ({exc}); eager steps", file=sys.stderr)
+                torch.cuda.synchronize(dev)
+        launches_per_step = plan.launches_per_run + 1   # + cs_scatter_gathered
         units_local = plan.P * upp
 
     for _ in range(args.warmup):
@@ -299,7 +343,8 @@ def run_ours(args):
     total_ms = float(sum(step_ms))
     sweep_avg = float(np.mean(sweep_ms))
     if world > 1:
-        t = torch.tensor([total_ms, sweep_avg], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms, sweep_avg], dtype=torch.float64,
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, sweep_avg = float(t[0]), float(t[1])
     value = P * upp * args.steps / (total_ms / 1e3)
@@ -317,11 +362,15 @@ def run_ours(args):
             "config": {"workload": WORKLOADS[args.workload][3], "n_apps": n, "pairs": P,
                        "configs_per_pair": upp, "budgets": [s.p_total for s in spaces],
                        "l2": "flushed before every step (256 MiB memset, outside the events)",
-                       "step": "CUDA graph: tables, solo, sweep, resolve, scatter",
+                       "step": ("CUDA graph: k_tables (+solo splits) -> k_sweep_tc3 (+decide, "
+                                "scatter) -> k_resolve (+decide)" if world == 1 else
+                                "shard sweep (3 kernels) -> ONE all-gather of the packed pair "
+                                f"records -> device scatter of the full matrix; {graph_mode}"),
                        "parallelism": f"pair shards x{world}"},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tf,
-                         "unit": "TFLOP/s", "frac": achieved_tflops / tf, "traffic": None,
-                         "kernel": {"tcgen05": "k_sweep_tc3<L,3,3> (tcgen05, A in TMEM, v4)",
+                         "unit": "TFLOP/s", "frac": achieved_tflops / tf,
+                         "traffic": measured_traffic(args.workload, args.kernel),
+                         "kernel": {"tcgen05": "k_sweep_tc3<L,4,2,3> (tcgen05, A in TMEM, v4)",
                                     "tcgen05_v3": "k_sweep_tc2<L,4,2> (tcgen05, A in TMEM, v3)",
                                     "simt": "k_sweep (SIMT fp32)",
                                     "tcgen05_smem": "k_sweep_tc (tcgen05, A in SMEM)"}.get(
@@ -334,8 +383,32 @@ def run_ours(args):
             "screen": {"queue_len": c.queue_len, "max_rel_gap": c.screen_error},
             "wall_s_timed_region": wall,
         }
-    # ---------------- e2e through the host-buffer C ABI (rank 0, 1 GPU) ----
-    if rank == 0 and not args.no_e2e:
+    # ---------------- e2e: host buffers in, result matrix out ----------------
+    if world > 1 and not args.no_e2e:
+        # every rank: pinned features -> H2D -> its shard -> NCCL all-gather ->
+        # full matrix; rank 0 reads the matrix back (the host matcher's input)
+        h_f = torch.from_numpy(np.ascontiguousarray(F)).pin_memory()
+        h_b = torch.from_numpy(np.ascontiguousarray(T)).pin_memory()
+        h_m = torch.empty((grid.n_budgets, n, n), dtype=torch.float64).pin_memory() \
+            if rank == 0 else None
+        for _ in range(2):
+            sh.run_host(h_f, h_b, h_m)
+        k = max(3, min(args.steps, 50))
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            sh.run_host(h_f, h_b, h_m)
+        mean_s = (time.perf_counter() - t0) / k
+        tt = torch.tensor([mean_s], dtype=torch.float64,
+                          device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            result["e2e"] = {"value": P * upp / float(tt[0]), "unit": "configs/s",
+                             "h2d_bytes_per_step": (F.nbytes + T.nbytes) * world,
+                             "d2h_bytes_per_step": h_m.numel() * 8, "steps": k, "n_apps": n,
+                             "api": "dist.ShardedSweep.run_host (pinned host in, NCCL all-gather, "
+                                    "matrix D2H on rank 0; max over ranks)"}
+    if world == 1 and not args.no_e2e:
         from paper_2405_03831_b200.host_abi import HostGraphCall
         from paper_2405_03831_b200 import matcher, scheduler
         n1, sp1 = spaces_for(args.workload)

@@ -237,6 +237,18 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
 int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,
                        int64_t pair_end, double *d_w, void *stream);
 
+/* --- multi-GPU record exchange (dist.py) -------------------------------- *
+ * A rank's pair records packed into ONE buffer (cap pairs per budget): weight
+ * f64 | corun_time f64 | corun_grid_index i32 | corun_chosen u8, each field
+ * budget-major with the rank's own pair count as row stride, 256-B aligned.
+ * Every rank's buffer has the same size, so one NCCL all-gather moves them
+ * all; cs_scatter_gathered then writes the symmetric L x N x N matrix from the
+ * gathered blocks (rank r owns pairs dist.shard_range(P, r, world)). */
+size_t cs_packed_records_bytes(int64_t cap, int32_t n_budgets);
+int cs_packed_records_layout(void *d_base, int64_t cap, int32_t n_budgets, cs_pair_out *out);
+int cs_scatter_gathered(const void *d_gathered, int32_t world, size_t rec_bytes, int64_t n_pairs,
+                        int32_t n_apps, int32_t n_budgets, double *d_w, void *stream);
+
 /* fnn.forward_batch on rows x 40 normalized inputs (fp64, unfloored). */
 int cs_forward_rows(const cs_network *net, const double *d_x, int64_t rows, double *d_y,
                     void *stream);

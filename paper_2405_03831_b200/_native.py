@@ -129,6 +129,12 @@ SWEEP_SYMBOLS = {
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_scatter_weights": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_packed_records_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32]),
+    "cs_packed_records_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                                ctypes.POINTER(CsPairOut)]),
+    "cs_scatter_gathered": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t,
+                                           ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_void_p, ctypes.c_void_p]),
     "cs_forward_rows": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_void_p]),
     "cs_device_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),

@@ -712,6 +712,33 @@ __global__ void k_scatter(const double *__restrict__ weight, int n, int64_t p_be
     }
 }
 
+// ---- k_scatter_gathered: the full matrix from an all-gathered record set ----
+// Rank r's block (rec_bytes each, world blocks back to back) holds its pair
+// shard dist.shard_range(P, r, world) in the packed layout of
+// cs_packed_records_layout: weight f64 [L][P_r] at offset 0, then the other
+// fields (unused here).  One thread per global pair.
+__global__ void k_scatter_gathered(const uint8_t *__restrict__ gathered, int world, int64_t rec_bytes,
+                                   int64_t P, int n, int L, double *__restrict__ W) {
+    const int64_t base = P / world, extra = P % world;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        // owner rank of pair p: the first `extra` ranks hold base + 1 pairs
+        const int64_t cut = extra * (base + 1);
+        const int64_t r = p < cut ? p / (base + 1) : extra + (p - cut) / base;
+        const int64_t b = r * base + (r < extra ? r : extra);
+        const int64_t Pr = base + (r < extra ? 1 : 0);
+        const double *w = reinterpret_cast<const double *>(gathered + r * rec_bytes);
+        int i, j;
+        pair_of(p, n, i, j);
+        for (int l = 0; l < L; ++l) {
+            const double v = w[(int64_t)l * Pr + (p - b)];
+            double *Wl = W + (size_t)l * n * n;
+            Wl[(size_t)i * n + j] = v;
+            Wl[(size_t)j * n + i] = v;
+        }
+    }
+}
+
 // ---- k_forward_rows: fnn.forward_batch, fp64 (fnn.py:161-165) -------------
 __global__ void k_forward_rows(const __grid_constant__ Net64P net, const double *__restrict__ x,
                                int64_t rows, double *__restrict__ y) {
@@ -1229,6 +1256,39 @@ int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begi
     int64_t blocks = (P + 255) / 256;
     if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
     k_scatter<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_weight, n_apps, pair_begin, P, d_w);
+    return check_launch();
+}
+
+size_t cs_packed_records_bytes(int64_t cap, int32_t n_budgets) {
+    if (cap < 0 || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS) return 0;
+    const size_t n = (size_t)cap * n_budgets;
+    return align256(8 * n) * 2 + align256(4 * n) + align256(n);
+}
+
+int cs_packed_records_layout(void *d_base, int64_t cap, int32_t n_budgets, cs_pair_out *out) {
+    if (!d_base || !out || ((uintptr_t)d_base & 255) || !cs_packed_records_bytes(cap, n_budgets))
+        return CS_ERR_ARG;
+    const size_t n = (size_t)cap * n_budgets;
+    char *p = (char *)d_base;
+    out->weight = (double *)p;
+    p += align256(8 * n);
+    out->corun_time = (double *)p;
+    p += align256(8 * n);
+    out->corun_grid_index = (int32_t *)p;
+    p += align256(4 * n);
+    out->corun_chosen = (uint8_t *)p;
+    return CS_OK;
+}
+
+int cs_scatter_gathered(const void *d_gathered, int32_t world, size_t rec_bytes, int64_t n_pairs,
+                        int32_t n_apps, int32_t n_budgets, double *d_w, void *stream) {
+    if (!d_gathered || !d_w || world < 1 || n_apps < 2 ||
+        n_pairs != (int64_t)n_apps * (n_apps - 1) / 2 || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS)
+        return CS_ERR_ARG;
+    int64_t blocks = (n_pairs + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+    k_scatter_gathered<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        (const uint8_t *)d_gathered, world, (int64_t)rec_bytes, n_pairs, n_apps, n_budgets, d_w);
     return check_launch();
 }
 

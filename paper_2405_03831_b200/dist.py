@@ -48,10 +48,12 @@ def gather_records(local: dict, P: int, group: Optional[dist.ProcessGroup] = Non
         padded[:, :n_local] = t
         # gather buffer laid out rank-major: (world, L, cap)
         buf = torch.empty((world, L, cap), dtype=dtype, device=t.device)
-        if hasattr(dist, "all_gather_into_tensor") and t.device.type == "cuda":
+        if t.device.type == "cuda" and dist.get_backend(group) == "nccl":
             dist.all_gather_into_tensor(buf, padded.contiguous(), group=group)
-        else:
-            dist.all_gather(list(buf.unbind(0)), padded.contiguous(), group=group)
+        else:   # gloo (CPU tests, or ranks sharing one GPU): stage through the host
+            host = [torch.empty((L, cap), dtype=dtype) for _ in range(world)]
+            dist.all_gather(host, padded.cpu().contiguous(), group=group)
+            buf.copy_(torch.stack(host))
         full = torch.empty((L, P), dtype=dtype, device=t.device)
         for r, (b, e) in enumerate(sizes):
             full[:, b:e] = buf[r, :, :e - b]
@@ -71,28 +73,81 @@ class ShardedSweep:
         self.n = n
         self.P = n * (n - 1) // 2
         b, e = shard_range(self.P, self.rank, self.world)
+        cap = max(e2 - b2 for b2, e2 in (shard_range(self.P, r, self.world)
+                                         for r in range(self.world)))
+        # the shard's records live in one packed buffer of the same size on every
+        # rank: the exchange is ONE all-gather (NCCL over NVLink), then one device
+        # scatter of the whole matrix from the gathered blocks
         self.plan = SweepPlan(weights, grid, n, b, e, device=device, with_matrix=False,
                               rel_eps=DEFAULT_REL_EPS if rel_eps is None else rel_eps,
-                              kernel=kernel)
+                              kernel=kernel, record_cap=cap)
+        self.cap = cap
+        self.gathered = torch.empty(self.world * self.plan.records.numel(), dtype=torch.uint8,
+                                    device=self.plan.device)
         self.matrix = torch.zeros((grid.n_budgets, n, n), dtype=torch.float64,
                                   device=self.plan.device)
 
-    def run(self, d_features, d_base_time, sweep_events=None) -> dict:
-        """Sweep the local shard, all-gather the records, scatter the full matrix."""
+    def run_host(self, h_features, h_base_time, h_matrix=None) -> None:
+        """End to end on this rank: pinned host inputs -> H2D -> shard sweep ->
+        all-gather -> full matrix -> D2H into `h_matrix` (pinned, rank 0 only
+        needs it; pass None elsewhere).  Synchronizes the stream."""
+        dev = self.plan.device
+        d_f = h_features.to(dev, non_blocking=True)
+        d_b = h_base_time.to(dev, non_blocking=True)
+        full = self.run(d_f, d_b)
+        if h_matrix is not None:
+            h_matrix.copy_(full, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    def exchange(self) -> None:
+        """All-gather the packed records of every shard and scatter the full matrix."""
         from . import _native as nat
         plan = self.plan
-        plan.launch(d_features, d_base_time, sweep_events)
-        P_loc = plan.P
-        local = {"corun_grid_index": plan.corun_grid_index[:, :P_loc],
-                 "corun_time": plan.corun_time[:, :P_loc],
-                 "corun_chosen": plan.corun_chosen[:, :P_loc],
-                 "weight": plan.weight[:, :P_loc]}
-        full = gather_records(local, self.P, self.group)
+        local = plan.records
+        if local.device.type == "cuda" and dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(self.gathered, local, group=self.group)
+        else:   # gloo (CPU tests, ranks sharing one GPU): stage through the host
+            host = [torch.empty_like(local, device="cpu") for _ in range(self.world)]
+            dist.all_gather(host, local.cpu(), group=self.group)
+            self.gathered.copy_(torch.cat(host))
         st = torch.cuda.current_stream(plan.device).cuda_stream
-        w = full["weight"].contiguous()
-        for l in range(plan.grid.n_budgets):
-            nat.check(plan.lib.cs_scatter_weights(w.data_ptr() + 8 * l * self.P, self.n, 0,
-                                                  self.P, self.matrix[l].data_ptr(), st),
-                      "cs_scatter_weights")
-        full["matrix"] = self.matrix
-        return full
+        nat.check(plan.lib.cs_scatter_gathered(self.gathered.data_ptr(), self.world,
+                                               local.numel(), self.P, self.n,
+                                               plan.grid.n_budgets, self.matrix.data_ptr(), st),
+                  "cs_scatter_gathered")
+
+    def run(self, d_features, d_base_time, sweep_events=None) -> torch.Tensor:
+        """Sweep the local shard, exchange, and return the full (L, N, N) matrix."""
+        self.plan.launch(d_features, d_base_time, sweep_events)
+        self.exchange()
+        return self.matrix
+
+    def records(self) -> dict:
+        """Full (L, P) record arrays (host-side reassembly of the gathered blocks)."""
+        plan = self.plan
+        L = plan.grid.n_budgets
+        blocks = self.gathered.view(self.world, -1)
+        out = {k: [] for k in ("corun_grid_index", "corun_time", "corun_chosen", "weight")}
+        for r in range(self.world):
+            b, e = shard_range(self.P, r, self.world)
+            Pr = e - b
+            base = blocks[r]
+            o = nat_layout(plan, self.cap, L)
+            for name, (off, dt, es) in o.items():
+                out[name].append(base[off:off + L * Pr * es].view(dt).view(L, Pr))
+        return {k: torch.cat(v, dim=1) for k, v in out.items()}
+
+
+def nat_layout(plan, cap: int, L: int) -> dict:
+    """Byte offsets of the packed record fields (cs_packed_records_layout)."""
+    import ctypes
+    from . import _native as nat
+    lay = nat.CsPairOut()
+    nat.check(plan.lib.cs_packed_records_layout(plan.records.data_ptr(), cap, L,
+                                                ctypes.byref(lay)), "cs_packed_records_layout")
+    base = plan.records.data_ptr()
+    addr = lambda p: ctypes.cast(p, ctypes.c_void_p).value - base
+    return {"weight": (addr(lay.weight), torch.float64, 8),
+            "corun_time": (addr(lay.corun_time), torch.float64, 8),
+            "corun_grid_index": (addr(lay.corun_grid_index), torch.int32, 4),
+            "corun_chosen": (addr(lay.corun_chosen), torch.uint8, 1)}

@@ -14,6 +14,7 @@ from __future__ import annotations
 import argparse
 import csv
 import io
+import json
 import os
 import subprocess
 from collections import OrderedDict
@@ -128,6 +129,9 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles"))
     ap.add_argument("--note", default="")
+    ap.add_argument("--traffic-key", default=None,
+                    help="WORKLOAD/KERNEL: record the first captured kernel's DRAM bytes "
+                         "(read + write) in profiles/traffic.json for bench.py's roofline")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     lp = a.launches or os.path.join(ROOT, "gpurun_out", f"launches_{a.tag}.csv")
@@ -143,6 +147,17 @@ def main():
             fh.write(f"# {a.tag}: `ncu --set full --clock-control none --import-source on` "
                      f"of the dominant kernel\n\n{a.note}\n\n")
             fh.write(full(rp) + "\n")
+        if a.traffic_key:
+            raw = list(csv.reader(io.StringIO(_ncu(rp, "--page", "raw", "--csv"))))
+            h, u, row = raw[0], raw[1], raw[2]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = sum(float(row[h.index(k)]) * scale.get(u[h.index(k)], 1)
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            path = os.path.join(a.out, "traffic.json")
+            d = json.load(open(path)) if os.path.exists(path) else {}
+            d[a.traffic_key] = tot
+            with open(path, "w") as fh:
+                json.dump(d, fh, indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
