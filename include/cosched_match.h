@@ -36,6 +36,14 @@ int cm_max_weight_matching(const double *w, int32_t n, int32_t *mate_out);
  * above, -3 if the matching came out imperfect (internal error). */
 int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out);
 
+/* The same with an explicit candidate degree: the blossom solver runs on the
+ * graph of each vertex's k lightest edges, then its LP dual is checked on ALL
+ * n(n-1)/2 edges (reduced cost >= 0, the reference's verify-optimum test);
+ * violating edges join the candidate set and the solve repeats, so the result
+ * is an optimum of the complete graph.  k <= 0 or k >= n - 1: the complete
+ * graph directly.  cm_min_weight_perfect_matching uses k = 24. */
+int cm_min_weight_perfect_matching_k(const double *w, int32_t n, int32_t k, int32_t *mate_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,3 +96,22 @@ def test_graph_csv(tmp_path):
     matcher.graph_to_csv(g, p)
     rows = p.read_text().splitlines()
     assert rows[0] == "i,j,weight,corun_flag" and len(rows) == 7
+
+
+@pytest.mark.parametrize("n,k", [(40, 1), (64, 2), (128, 4), (200, 24)])
+def test_sparse_candidates_plus_certificate_equal_dense(n, k):
+    """cm_min_weight_perfect_matching_k: a starved candidate graph (k lightest
+    edges per vertex, possibly without any perfect matching) must still end at
+    the complete graph's optimum via the dual certificate / edge-addition loop."""
+    from paper_2405_03831_b200 import _native as nat
+    for seed in range(3):
+        W = random_graph(n, 100 + seed)
+        g = matcher.PairGraph(W)
+        out = {}
+        for kk in (k, 0):
+            mate = np.empty(n, dtype=np.int32)
+            rc = nat.match_lib().cm_min_weight_perfect_matching_k(
+                nat.ptr(np.ascontiguousarray(W)), n, kk, nat.ptr(mate, nat.c_int32_p))
+            assert rc == 0
+            out[kk] = sorted((v, int(mate[v])) for v in range(n) if v < mate[v])
+        assert out[k] == out[0]
