@@ -44,6 +44,19 @@ int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out
  * graph directly.  cm_min_weight_perfect_matching uses k = 24. */
 int cm_min_weight_perfect_matching_k(const double *w, int32_t n, int32_t k, int32_t *mate_out);
 
+/* Minimum-weight perfect matching given vertex potentials with
+ * w[u][v] <= pot[u] + pot[v] for every pair -- the pair graph of the sweep
+ * has them: a pair's weight is min(co-run, solo_u + solo_v), so pot = the
+ * per-app solo times.  Every perfect matching pays sum(pot) minus its
+ * "benefit" pot[u] + pot[v] - w[u][v] >= 0, so the optimum is a MAXIMUM-weight
+ * matching of the benefit graph (only positive edges: pairs that co-run
+ * profitably), certified as above, with the leftover vertices paired in index
+ * order (zero benefit between them).  This removes the massive degeneracy of
+ * time-share pairs (all perfect matchings of them weigh the same), which makes
+ * the direct solve slow.  Returns -4 if `pot` is not a bound. */
+int cm_min_weight_perfect_matching_pot(const double *w, int32_t n, const double *pot, int32_t k,
+                                       int32_t *mate_out);
+
 #ifdef __cplusplus
 }
 #endif

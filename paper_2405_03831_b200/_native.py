@@ -153,6 +153,8 @@ MATCH_SYMBOLS = {
     "cm_min_weight_perfect_matching": (ctypes.c_int, [c_double_p, ctypes.c_int32, c_int32_p]),
     "cm_min_weight_perfect_matching_k": (ctypes.c_int, [c_double_p, ctypes.c_int32, ctypes.c_int32,
                                                         c_int32_p]),
+    "cm_min_weight_perfect_matching_pot": (ctypes.c_int, [c_double_p, ctypes.c_int32, c_double_p,
+                                                          ctypes.c_int32, c_int32_p]),
 }
 
 

@@ -482,17 +482,37 @@ private:
     std::vector<size_t> touched_;
 };
 
-// power-of-two shift that turns every (reflected) weight into an exact integer
-int choose_shift(const double *w, int n, double reflect, bool use_reflect, int *shift) {
+// The value of edge (u, v) the blossom solver maximizes, as a double:
+//   REFLECT: (max w + 1) - w[u][v]          (matcher.py:84-85; complete graph, perfect)
+//   BENEFIT: pot[u] + pot[v] - w[u][v]       (only edges with a positive value exist)
+//   RAW:     w[u][v]
+struct EdgeValue {
+    enum Kind { RAW, REFLECT, BENEFIT } kind;
+    const double *w;
+    int n;
+    double reflect;
+    const double *pot;
+    double operator()(int u, int v) const {
+        const double x = w[(size_t)u * n + v];
+        switch (kind) {
+            case REFLECT: return reflect - x;
+            case BENEFIT: return (pot[u] + pot[v]) - x;
+            default: return x;
+        }
+    }
+    bool exists(double x) const { return kind != BENEFIT || x > 0.0; }
+};
+
+// power-of-two shift that turns every edge value into an exact integer
+// (-2 when they span too many binary orders of magnitude for 128 bits)
+int choose_shift(const EdgeValue &f, int *shift) {
     int emin = INT32_MAX, emax = INT32_MIN;
-    for (int u = 0; u < n; ++u)
-        for (int v = 0; v < n; ++v) {
+    for (int u = 0; u < f.n; ++u)
+        for (int v = 0; v < f.n; ++v) {
             if (u == v) continue;
-            double x = w[(size_t)u * n + v];
-            if (!std::isfinite(x)) return -1;
-            if (x != w[(size_t)v * n + u]) return -1;
-            double r = use_reflect ? reflect - x : x;
-            if (r == 0.0) continue;
+            const double r = f(u, v);
+            if (!std::isfinite(r)) return -1;
+            if (r == 0.0 || !f.exists(r)) continue;
             int e;
             std::frexp(r, &e);
             emin = std::min(emin, e);
@@ -505,34 +525,13 @@ int choose_shift(const double *w, int n, double reflect, bool use_reflect, int *
     return 0;
 }
 
-// scaled integer weight of (reflected) entry x
-inline i128 scaled(double x, double reflect, bool use_reflect, int shift) {
-    return (i128)std::ldexp(use_reflect ? reflect - x : x, shift);
-}
+inline i128 scaled(double x, int shift) { return (i128)std::ldexp(x, shift); }
 
-Graph dense_graph(const double *w, int n, double reflect, bool use_reflect, int shift) {
+// symmetric CSR graph over an undirected edge set (pairs u < v)
+Graph make_graph(const EdgeValue &f, const std::vector<std::pair<int, int>> &edges, int shift) {
     Graph g;
-    g.n = n;
-    g.off.resize(n + 1);
-    g.nbr.reserve((size_t)n * (n - 1));
-    g.w.reserve((size_t)n * (n - 1));
-    for (int u = 0; u < n; ++u) {
-        g.off[u] = (int64_t)g.nbr.size();
-        for (int v = 0; v < n; ++v) {
-            if (v == u) continue;
-            g.nbr.push_back(v);
-            g.w.push_back(scaled(w[(size_t)u * n + v], reflect, use_reflect, shift));
-        }
-    }
-    g.off[n] = (int64_t)g.nbr.size();
-    return g;
-}
-
-// symmetric CSR graph from an undirected edge set (pairs u < v)
-Graph sparse_graph(const double *w, int n, const std::vector<std::pair<int, int>> &edges,
-                   double reflect, int shift) {
-    Graph g;
-    g.n = n;
+    g.n = f.n;
+    const int n = f.n;
     std::vector<int64_t> deg(n + 1, 0);
     for (auto &e : edges) { ++deg[e.first]; ++deg[e.second]; }
     g.off.assign(n + 1, 0);
@@ -541,24 +540,24 @@ Graph sparse_graph(const double *w, int n, const std::vector<std::pair<int, int>
     g.w.resize(g.off[n]);
     std::vector<int64_t> pos(g.off.begin(), g.off.end() - 1);
     for (auto &e : edges) {
-        const i128 x = scaled(w[(size_t)e.first * n + e.second], reflect, true, shift);
+        const i128 x = scaled(f(e.first, e.second), shift);
         g.nbr[pos[e.first]] = e.second; g.w[pos[e.first]++] = x;
         g.nbr[pos[e.second]] = e.first; g.w[pos[e.second]++] = x;
     }
     return g;
 }
 
-// Edges (i, j) of the complete graph whose reduced cost under the solver's
-// final duals is negative: y_i + y_j + 2 * (sum of duals of blossoms holding
-// both) - 2 w_ij < 0 in the solver's doubled units (networkx / reference
-// verify_optimum).  Returns up to `per_vertex` most violated edges per vertex.
-std::vector<std::pair<int, int>> violations(const Blossom &m, const double *w, int n,
-                                            double reflect, int shift, int per_vertex) {
+// Existing edges (i, j) whose reduced cost under the solver's final duals is
+// negative: y_i + y_j + 2 * (sum of duals of blossoms holding both) - 2 w_ij < 0
+// in the solver's doubled units (the reference's verify_optimum).  Up to
+// `per_vertex` most violated edges per vertex.
+std::vector<std::pair<int, int>> violations(const Blossom &m, const EdgeValue &f, int shift,
+                                            int per_vertex) {
+    const int n = f.n;
     const std::vector<i128> &dual = m.duals();
     const std::vector<int> &parent = m.parents();
     const int extra = m.extra();
-    // each vertex's chain of enclosing blossoms, outermost first
-    std::vector<std::vector<int>> chain(n);
+    std::vector<std::vector<int>> chain(n);   // enclosing blossoms, outermost first
     for (int v = 0; v < n; ++v) {
         for (int b = parent[v]; b >= 0; b = parent[b]) chain[v].push_back(b);
         std::reverse(chain[v].begin(), chain[v].end());
@@ -569,11 +568,12 @@ std::vector<std::pair<int, int>> violations(const Blossom &m, const double *w, i
         worst.clear();
         for (int j = 0; j < n; ++j) {
             if (j == i) continue;
+            const double x = f(i, j);
+            if (!f.exists(x)) continue;
             i128 z = 0;
             const auto &ci = chain[i], &cj = chain[j];
             for (size_t k = 0; k < ci.size() && k < cj.size() && ci[k] == cj[k]; ++k) z += dual[ci[k]];
-            const i128 red = dual[i] + dual[j] + 2 * z -
-                             2 * (scaled(w[(size_t)i * n + j], reflect, true, shift) << extra);
+            const i128 red = dual[i] + dual[j] + 2 * z - 2 * (scaled(x, shift) << extra);
             if (red < 0) worst.push_back({red, j});
         }
         if (worst.size() > (size_t)per_vertex) {
@@ -587,23 +587,69 @@ std::vector<std::pair<int, int>> violations(const Blossom &m, const double *w, i
     return out;
 }
 
+// Maximum-weight matching of the graph of existing edges of `f`: the blossom
+// solver on the k most valuable edges of every vertex (k <= 0: all), then the
+// dual certificate on every existing edge, adding violators until none is
+// left.  Returns 0 or -3.
+int certified_matching(const EdgeValue &f, int k, int shift, int32_t *mate_out) {
+    const int n = f.n;
+    std::vector<std::pair<int, int>> edges;
+    std::vector<std::pair<double, int>> row(n);
+    for (int u = 0; u < n; ++u) {
+        int c = 0;
+        for (int v = 0; v < n; ++v) {
+            if (v == u) continue;
+            const double x = f(u, v);
+            if (f.exists(x)) row[c++] = {-x, v};
+        }
+        const int take = (k <= 0 || k >= c) ? c : k;
+        std::partial_sort(row.begin(), row.begin() + take, row.begin() + c);
+        for (int q = 0; q < take; ++q) edges.push_back({std::min(u, row[q].second), std::max(u, row[q].second)});
+    }
+    std::sort(edges.begin(), edges.end());
+    edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+    for (int round = 0; round < 64; ++round) {
+        const Graph g = make_graph(f, edges, shift);
+        Blossom m(g);
+        m.run(false);
+        const std::vector<std::pair<int, int>> bad =
+            (k <= 0) ? std::vector<std::pair<int, int>>() : violations(m, f, shift, 8);
+        if (bad.empty()) {
+            for (int v = 0; v < n; ++v) mate_out[v] = m.mate()[v];
+            return 0;
+        }
+        edges.insert(edges.end(), bad.begin(), bad.end());
+        std::sort(edges.begin(), edges.end());
+        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+    }
+    return -3;
+}
+
+int check_square(const double *w, int32_t n) {
+    for (int u = 0; u < n; ++u)
+        for (int v = 0; v < n; ++v) {
+            const double x = w[(size_t)u * n + v];
+            if (!std::isfinite(x)) return -1;
+            if (u != v && x != w[(size_t)v * n + u]) return -1;
+        }
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
 
-const char *cm_version(void) { return "cosched_match 0.2.0 (exact int128 blossom, sparse + dual certificate)"; }
+const char *cm_version(void) { return "cosched_match 0.3.0 (exact int128 blossom, sparse + dual certificate)"; }
 
 int cm_max_weight_matching(const double *w, int32_t n, int32_t *mate_out) {
     if (n < 0 || (n > 0 && (!w || !mate_out))) return -1;
     if (n == 0) return 0;
+    if (check_square(w, n)) return -1;
+    EdgeValue f{EdgeValue::RAW, w, n, 0.0, nullptr};
     int shift = 0;
-    int rc = choose_shift(w, n, 0.0, false, &shift);
+    int rc = choose_shift(f, &shift);
     if (rc) return rc;
-    const Graph g = dense_graph(w, n, 0.0, false, shift);
-    Blossom m(g);
-    m.run(false);
-    for (int v = 0; v < n; ++v) mate_out[v] = m.mate()[v];
-    return 0;
+    return certified_matching(f, 0, shift, mate_out);
 }
 
 int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out) {
@@ -612,49 +658,46 @@ int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out
 
 int cm_min_weight_perfect_matching_k(const double *w, int32_t n, int32_t k, int32_t *mate_out) {
     if (n < 2 || (n & 1) || !w || !mate_out) return -1;
+    if (check_square(w, n)) return -1;
     double mx = -INFINITY;
-    for (size_t q = 0; q < (size_t)n * n; ++q) {
-        if (!std::isfinite(w[q])) return -1;
-        mx = std::max(mx, w[q]);
-    }
-    const double reflect = mx + 1.0;     // matcher.py:84
+    for (size_t q = 0; q < (size_t)n * n; ++q) mx = std::max(mx, w[q]);
+    EdgeValue f{EdgeValue::REFLECT, w, n, mx + 1.0, nullptr};   // matcher.py:84
     int shift = 0;
-    int rc = choose_shift(w, n, reflect, true, &shift);
+    int rc = choose_shift(f, &shift);
     if (rc) return rc;
-    // candidates: the k lightest edges of every vertex (k <= 0 or >= n-1: all)
-    std::vector<std::pair<int, int>> edges;
-    if (k <= 0 || k >= n - 1) {
-        for (int u = 0; u < n; ++u)
-            for (int v = u + 1; v < n; ++v) edges.push_back({u, v});
-    } else {
-        std::vector<std::pair<double, int>> row(n - 1);
-        for (int u = 0; u < n; ++u) {
-            int c = 0;
-            for (int v = 0; v < n; ++v)
-                if (v != u) row[c++] = {w[(size_t)u * n + v], v};
-            std::partial_sort(row.begin(), row.begin() + k, row.end());
-            for (int q = 0; q < k; ++q) edges.push_back({std::min(u, row[q].second), std::max(u, row[q].second)});
-        }
-        std::sort(edges.begin(), edges.end());
-        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+    rc = certified_matching(f, k, shift, mate_out);
+    if (rc) return rc;
+    for (int v = 0; v < n; ++v)
+        if (mate_out[v] < 0) return -3;
+    return 0;
+}
+
+int cm_min_weight_perfect_matching_pot(const double *w, int32_t n, const double *pot, int32_t k,
+                                       int32_t *mate_out) {
+    if (n < 2 || (n & 1) || !w || !pot || !mate_out) return -1;
+    if (check_square(w, n)) return -1;
+    for (int u = 0; u < n; ++u) {
+        if (!std::isfinite(pot[u])) return -1;
+        for (int v = 0; v < n; ++v)
+            if (u != v && w[(size_t)u * n + v] > pot[u] + pot[v]) return -4;   // not a potential bound
     }
-    for (int round = 0; round < 64; ++round) {
-        const Graph g = sparse_graph(w, n, edges, reflect, shift);
-        Blossom m(g);
-        m.run(false);
-        const std::vector<std::pair<int, int>> bad = violations(m, w, n, reflect, shift, 8);
-        if (bad.empty()) {
-            for (int v = 0; v < n; ++v) {
-                mate_out[v] = m.mate()[v];
-                if (mate_out[v] < 0) return -3;
-            }
-            return 0;
-        }
-        edges.insert(edges.end(), bad.begin(), bad.end());
-        std::sort(edges.begin(), edges.end());
-        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+    EdgeValue f{EdgeValue::BENEFIT, w, n, 0.0, pot};
+    int shift = 0;
+    int rc = choose_shift(f, &shift);
+    if (rc) return rc;
+    rc = certified_matching(f, k, shift, mate_out);
+    if (rc) return rc;
+    // vertices left single pair up in index order: between two of them the
+    // benefit is 0, so any pairing completes an optimal perfect matching
+    int prev = -1;
+    for (int v = 0; v < n; ++v) {
+        if (mate_out[v] >= 0) continue;
+        if (prev < 0) { prev = v; continue; }
+        mate_out[prev] = v;
+        mate_out[v] = prev;
+        prev = -1;
     }
-    return -3;
+    return prev < 0 ? 0 : -3;
 }
 
 }  // extern "C"

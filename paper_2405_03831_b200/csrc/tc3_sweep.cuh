@@ -25,12 +25,15 @@ namespace tc3 {
 //           128 threads arriving;
 // V bit 1: one MMA-issuer warp per group instead of one shared issuer;
 // V bit 2: no issuer warps -- the group's own compute warps take turns (warp
-//          c % 4 issues config c), so 4 warps per scheduler get 128 registers.
+//          c % 4 issues config c), so 4 warps per scheduler get 128 registers;
+// V bit 3: the issuer warps poll a_ready (try_wait without a suspend hint).
 template <int G, int S, int V = 0>
 struct Cfg {
     static constexpr bool kElected = (V & 1) != 0;
     static constexpr bool kPerGroupIssuer = (V & 2) != 0;
     static constexpr bool kComputeIssue = (V & 4) != 0;
+    static constexpr bool kIssuerSpin = (V & 8) != 0;   // issuer polls instead of sleeping
+    static constexpr bool kNoTensor = (V & 16) != 0;    // TIMING PROBE ONLY: no MMAs, no waits
     static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
     static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
@@ -58,6 +61,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
     if (mbar_try_sleep(bar, parity)) return;
     const long long t0 = clock64();
     while (!mbar_try_sleep(bar, parity)) {
+        if (clock64() - t0 > 4000000000LL) __trap();
+    }
+}
+
+// warp-uniform wait: the exit test is a warp vote, so the warp leaves the
+// loop converged and the .sync.aligned tcgen05 ops that follow need no
+// __syncwarp (bounded like tc::mbar_wait)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t *bar, uint32_t parity) {
+    if (__all_sync(0xffffffffu, tc::mbar_try(bar, parity))) return;
+    const long long t0 = clock64();
+    while (!__all_sync(0xffffffffu, tc::mbar_try(bar, parity))) {
         if (clock64() - t0 > 4000000000LL) __trap();
     }
 }
@@ -211,7 +225,9 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     const int64_t total_groups = (int64_t)gridDim.x * G;
     const int n_cfg = a.g.G;
 
-    if (!C::kComputeIssue && g >= G) {
+    if (C::kNoTensor && g >= G) {
+        // timing probe: CUDA-core work only (results are garbage)
+    } else if (!C::kComputeIssue && g >= G) {
         // ===== one MMA-issuer warp serves the G groups in lockstep =====
         // Every active group of a round sweeps the same configs in the same
         // order, so the issuer visits (config k, group q) round-robin.
@@ -228,7 +244,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             for (int k = 0; k < n_cfg; ++k) {
                 for (int q = q_lo; q < q_hi; ++q) {
                     const int b = q * S + st;
-                    if (C::kPerGroupIssuer) tc3::mbar_wait_sleep(&a_ready[b], (ph >> b) & 1u);
+                    if (C::kPerGroupIssuer && !C::kIssuerSpin) tc3::mbar_wait_sleep(&a_ready[b], (ph >> b) & 1u);
                     else tc::mbar_wait(&a_ready[b], (ph >> b) & 1u);
                     ph ^= 1u << b;
                     __syncwarp();
@@ -294,9 +310,8 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
 
             // epilogue of config c from stage s (s compile-time after unrolling)
             auto epilogue = [&](int c, int s) {
-                tc::mbar_wait(&dr[s], ph[s]);
+                if (!C::kNoTensor) tc3::mbar_wait_warp(&dr[s], ph[s]);
                 ph[s] ^= 1u;
-                __syncwarp();
                 tc::fence_after();
                 const float y = tc3::head_from_tmem(td[s], wo2, bo);
                 const int cl = y < 0.5f;

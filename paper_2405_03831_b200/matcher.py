@@ -87,12 +87,26 @@ def _check_perfect(n: int, pairs) -> None:
 
 
 def min_weight_perfect_matching(graph: PairGraph) -> list:
-    """Perfect matching of minimum total weight, as sorted (i, j) pairs."""
+    """Perfect matching of minimum total weight, as sorted (i, j) pairs.
+
+    A graph built by the GPU sweep carries per-app potentials (the solo times,
+    ``PairDecisions.potentials``): the native solver then maximizes the
+    co-run benefit instead (cm_min_weight_perfect_matching_pot), which avoids
+    the degeneracy of the many equal-weight time-share pairings.  Either way
+    the result is a certified optimum of the complete graph (LP dual check)."""
     n = graph.n
     lib = nat.match_lib()
     w = np.ascontiguousarray(graph.weights, dtype=np.float64)
     mate = np.empty(n, dtype=np.int32)
-    rc = lib.cm_min_weight_perfect_matching(nat.ptr(w), n, nat.ptr(mate, nat.c_int32_p))
+    pot_fn = getattr(graph.decisions, "potentials", None)
+    rc = None
+    if pot_fn is not None:
+        pot = pot_fn()
+        k = 64 if n <= 256 else 24
+        rc = lib.cm_min_weight_perfect_matching_pot(nat.ptr(w), n, nat.ptr(pot), k,
+                                                    nat.ptr(mate, nat.c_int32_p))
+    if rc is None or rc == -4:
+        rc = lib.cm_min_weight_perfect_matching(nat.ptr(w), n, nat.ptr(mate, nat.c_int32_p))
     if rc == -2:
         raise ValidationError("edge weights span too many orders of magnitude for exact matching")
     if rc != 0:

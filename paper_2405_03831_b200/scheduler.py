@@ -62,6 +62,12 @@ class PairDecisions(Mapping):
     def __len__(self) -> int:
         return self._n * (self._n - 1) // 2
 
+    def potentials(self) -> np.ndarray:
+        """Per-app best solo times: every pair weight is min(co-run, solo_i +
+        solo_j) <= pot_i + pot_j, which the native matcher uses to solve the
+        benefit form of the matching (cm_min_weight_perfect_matching_pot)."""
+        return np.ascontiguousarray(self._r.solo_time[self._l], dtype=np.float64)
+
     def __iter__(self):
         n = self._n
         for i in range(n):

@@ -115,3 +115,37 @@ def test_sparse_candidates_plus_certificate_equal_dense(n, k):
             assert rc == 0
             out[kk] = sorted((v, int(mate[v])) for v in range(n) if v < mate[v])
         assert out[k] == out[0]
+
+
+def test_potential_form_equals_direct_on_sweep_graphs():
+    """cm_min_weight_perfect_matching_pot (benefit form, solo-time potentials)
+    reaches the same optimum as the direct solve on real pair graphs (oracle
+    sweep of the synthetic workload), and rejects potentials that do not bound
+    the weights."""
+    import oracle
+    from conftest import workload
+    from paper_2405_03831_b200 import _native as nat, core, fnn
+    from paper_2405_03831_b200.grid import KnobGrid
+    w = fnn.load_weights(os.path.join(GOLDEN, "weights.json"))
+    for n, budget in ((64, 400.0), (150, 350.0)):
+        F, T = workload(n, 3)
+        r = oracle.sweep(w, F, T, KnobGrid([core.default_space(budget)]))
+        W = np.zeros((n, n))
+        iu, ju = np.triu_indices(n, 1)
+        W[iu, ju] = r["weight"][0]
+        W = np.ascontiguousarray(W + W.T)
+        pot = np.ascontiguousarray(r["solo_time"][0])
+        g = matcher.PairGraph(W)
+        out = {}
+        for name, call in (("pot", lambda m: nat.match_lib().cm_min_weight_perfect_matching_pot(
+                                nat.ptr(W), n, nat.ptr(pot), 8, nat.ptr(m, nat.c_int32_p))),
+                           ("direct", lambda m: nat.match_lib().cm_min_weight_perfect_matching_k(
+                                nat.ptr(W), n, 0, nat.ptr(m, nat.c_int32_p)))):
+            mate = np.empty(n, dtype=np.int32)
+            assert call(mate) == 0
+            out[name] = matcher.matching_weight(g, [(v, int(mate[v])) for v in range(n) if v < mate[v]])
+        assert abs(out["pot"] - out["direct"]) <= 1e-12 * out["direct"]
+        bad = np.ascontiguousarray(pot * 0.4)
+        mate = np.empty(n, dtype=np.int32)
+        assert nat.match_lib().cm_min_weight_perfect_matching_pot(
+            nat.ptr(W), n, nat.ptr(bad), 8, nat.ptr(mate, nat.c_int32_p)) == -4
