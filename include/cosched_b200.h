@@ -263,7 +263,11 @@ int cs_device_free(void *d_ptr);
 size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid);
 /* h_weights: L x N x N (NULL to skip); h_pairs members: L x P host arrays
  * (NULL members skipped); h_solo members: L x N host arrays (NULL skipped);
- * h_clamps: L (NULL to skip).  Full graph (all P pairs). */
+ * h_clamps: L (NULL to skip).  Full graph (all P pairs).  The knob grid, the
+ * network image and the zeroed matrix persist in d_workspace: a call that
+ * repeats the previous call's grid/network on the same workspace uploads only
+ * the per-call inputs (a host-side record per workspace pointer; the
+ * workspace must not be written by anything else between calls). */
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                         const double *h_base_time, int32_t n_apps, double rel_eps,
                         void *d_workspace, size_t workspace_bytes, double *h_weights,

@@ -28,6 +28,9 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
 
 namespace {
 
@@ -1380,14 +1383,49 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
 #define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
     CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
     CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    if (G) {
-        CS_TRY(cudaMemcpyAsync(ws + L.knob1, h_grid->knob1, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
-        CS_TRY(cudaMemcpyAsync(ws + L.knob2, h_grid->knob2, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
-        CS_TRY(cudaMemcpyAsync(ws + L.mask, h_grid->mask, sizeof(uint32_t) * G, cudaMemcpyHostToDevice, st));
+    // The knob grid, the network image and the zeroed matrix persist in the
+    // workspace between calls: re-upload only what changed since the last
+    // call on this workspace (host-side record per workspace pointer).
+    std::vector<uint8_t> key;
+    {
+        auto put = [&key](const void *p, size_t bytes) {
+            const uint8_t *b = (const uint8_t *)p;
+            key.insert(key.end(), b, b + bytes);
+        };
+        const int32_t dims[4] = {n_apps, nb, G, S};
+        put(dims, sizeof(dims));
+        if (G) {
+            put(h_grid->knob1, sizeof(double) * G * 4);
+            put(h_grid->knob2, sizeof(double) * G * 4);
+            put(h_grid->mask, sizeof(uint32_t) * G);
+        }
+        if (S) put(h_grid->solo_knob, sizeof(double) * S * 4);
+        Net64P np;
+        if (!net64_from(net, &np)) return CS_ERR_ARG;
+        put(&np, sizeof(np));
+        put(&workspace_bytes, sizeof(workspace_bytes));
     }
-    if (S) CS_TRY(cudaMemcpyAsync(ws + L.solo_knob, h_grid->solo_knob, sizeof(double) * S * 4, cudaMemcpyHostToDevice, st));
-    CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, sizeof(uint32_t) * 2, st));
-    CS_TRY(cudaMemsetAsync(ws + L.clamps, 0, sizeof(unsigned long long) * nb, st));
+    static std::mutex cache_mu;
+    static std::unordered_map<const void *, std::vector<uint8_t>> cache;
+    bool fresh;
+    {
+        std::lock_guard<std::mutex> lock(cache_mu);
+        auto it = cache.find(d_workspace);
+        fresh = it == cache.end() || it->second != key;
+        if (fresh) cache[d_workspace] = key;   // recorded before the upload: a failure below
+    }                                           // returns an error and the caller retries
+    if (fresh) {
+        if (G) {
+            CS_TRY(cudaMemcpyAsync(ws + L.knob1, h_grid->knob1, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
+            CS_TRY(cudaMemcpyAsync(ws + L.knob2, h_grid->knob2, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
+            CS_TRY(cudaMemcpyAsync(ws + L.mask, h_grid->mask, sizeof(uint32_t) * G, cudaMemcpyHostToDevice, st));
+        }
+        if (S) CS_TRY(cudaMemcpyAsync(ws + L.solo_knob, h_grid->solo_knob, sizeof(double) * S * 4, cudaMemcpyHostToDevice, st));
+        // the sweep writes every off-diagonal entry each call; the diagonal stays 0
+        CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n * nb, st));
+    }
+    // queue counters and clamp counters are adjacent: one memset
+    CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, (L.clamps - L.qcount) + sizeof(unsigned long long) * nb, st));
 
     cs_grid dg = *h_grid;
     dg.knob1 = (const double *)(ws + L.knob1);
@@ -1396,14 +1434,13 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     dg.solo_knob = (const double *)(ws + L.solo_knob);
     cs_tables t;
     CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
-    CS_RC(cs_tables_set_network(net, &t, stream));
+    if (fresh) CS_RC(cs_tables_set_network(net, &t, stream));
     cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
                    (int32_t *)(ws + L.solo_clamps)};
     CS_RC(cs_prepare(net, (const double *)(ws + L.feats), (const double *)(ws + L.bt), n_apps, &dg,
                      &t, so, stream));
     cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
-    if (h_weights) CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n * nb, st));
     CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
                               so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue),
                               (uint32_t *)(ws + L.qcount), (unsigned long long *)(ws + L.clamps),

@@ -83,10 +83,9 @@ class HostGraphCall:
         self.h_clamps = np.zeros(L, dtype=np.uint64)
 
     def bytes_per_call(self) -> tuple:
-        """(H2D bytes, D2H bytes) moved by one call."""
-        g = self.grid
-        h2d = self.h_features.nbytes + self.h_base_time.nbytes + 2 * g.n_grid * 32 + g.n_grid * 4 \
-            + len(g.solo_knob) * 32
+        """(H2D bytes, D2H bytes) moved by one repeated call (the grid and the
+        network stay in the workspace after the first call)."""
+        h2d = self.h_features.nbytes + self.h_base_time.nbytes
         d2h = self.h_weights.nbytes + self.h_solo_time.nbytes + self.h_solo_split.nbytes + \
             self.h_clamps.nbytes
         if self.with_records:
