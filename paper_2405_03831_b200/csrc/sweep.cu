@@ -1362,6 +1362,28 @@ size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid) {
     return graph_layout(n_apps, h_grid).total;
 }
 
+namespace {
+// The per-call part of cs_build_graph_host (everything after the cached
+// uploads): enqueue only, no synchronization -- so it can be captured.
+int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const double *h_features,
+                       const double *h_base_time, int32_t n_apps, double rel_eps, char *ws,
+                       const GraphLayout &L, double *h_weights, cs_pair_out h_pairs,
+                       cs_solo_out h_solo, unsigned long long *h_clamps, bool set_net,
+                       cudaStream_t st);
+
+struct HostCallKey {
+    const void *ws, *f, *bt, *w, *p0, *p1, *p2, *p3, *s0, *s1, *s2, *cl, *stream;
+    int32_t n;
+    double eps;
+    bool operator==(const HostCallKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct HostCallGraph {
+    HostCallKey key;
+    cudaGraphExec_t exec = nullptr;
+    int hits = 0;
+};
+}  // namespace
+
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                         const double *h_base_time, int32_t n_apps, double rel_eps,
                         void *d_workspace, size_t workspace_bytes, double *h_weights,
@@ -1381,8 +1403,6 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
 #define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { \
         fprintf(stderr, "cosched_b200: %s\n", cudaGetErrorString(_e)); return CS_ERR_CUDA; } } while (0)
 #define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
-    CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
-    CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     // The knob grid, the network image and the zeroed matrix persist in the
     // workspace between calls: re-upload only what changed since the last
     // call on this workspace (host-side record per workspace pointer).
@@ -1424,6 +1444,89 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
         // the sweep writes every off-diagonal entry each call; the diagonal stays 0
         CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n * nb, st));
     }
+    if (fresh) {
+        // network image into the workspace's tables (pageable copy, outside any graph)
+        cs_tables t;
+        CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
+        CS_RC(cs_tables_set_network(net, &t, stream));
+    }
+    // Per-call work: replayed as a CUDA graph once the same call (workspace,
+    // host buffers, stream) repeats -- one launch instead of ~15 API calls.
+    // Host buffers must be pinned for the graph (a capture with pageable
+    // memory fails and the call stays on the direct path).
+    HostCallKey key2{d_workspace, h_features, h_base_time, h_weights,
+                     h_pairs.corun_grid_index, h_pairs.corun_time, h_pairs.corun_chosen,
+                     h_pairs.weight, h_solo.solo_time, h_solo.solo_split, h_solo.solo_clamps,
+                     h_clamps, stream, n_apps, rel_eps};
+    static std::mutex graph_mu;
+    static std::vector<HostCallGraph> graphs;
+    cudaGraphExec_t exec = nullptr;
+    bool try_capture = false;
+    if (fresh) {
+        // new grid / network on this workspace: graphs captured for it carry
+        // stale kernel parameters (the fp32 head weights ride in them)
+        std::lock_guard<std::mutex> lock(graph_mu);
+        for (auto it = graphs.begin(); it != graphs.end();) {
+            if (it->key.ws == d_workspace) {
+                if (it->exec) cudaGraphExecDestroy(it->exec);
+                it = graphs.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    } else {
+        std::lock_guard<std::mutex> lock(graph_mu);
+        for (auto &g : graphs)
+            if (g.key == key2) { if (g.exec) exec = g.exec; else if (++g.hits == 1) try_capture = true; }
+        if (!exec && !try_capture) { graphs.push_back(HostCallGraph{key2, nullptr, 0}); }
+    }
+    if (exec) {
+        CS_TRY(cudaGraphLaunch(exec, st));
+    } else if (try_capture) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        int erc = ok ? enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
+                                          h_weights, h_pairs, h_solo, h_clamps, false, st)
+                     : CS_ERR_CUDA;
+        if (ok) ok = cudaStreamEndCapture(st, &graph) == cudaSuccess && erc == CS_OK;
+        if (ok) ok = cudaGraphInstantiate(&ge, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        {
+            std::lock_guard<std::mutex> lock(graph_mu);
+            for (auto &g : graphs)
+                if (g.key == key2) { g.exec = ok ? ge : nullptr; g.hits = ok ? 1 : 1 << 30; }
+        }
+        if (ok) CS_TRY(cudaGraphLaunch(ge, st));
+        else CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
+                                      h_weights, h_pairs, h_solo, h_clamps, false, st));
+    } else {
+        CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
+                                 h_weights, h_pairs, h_solo, h_clamps, false, st));
+    }
+    CS_TRY(cudaStreamSynchronize(st));
+#undef CS_TRY
+#undef CS_RC
+    return CS_OK;
+}
+
+namespace {
+int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const double *h_features,
+                       const double *h_base_time, int32_t n_apps, double rel_eps, char *ws,
+                       const GraphLayout &L, double *h_weights, cs_pair_out h_pairs,
+                       cs_solo_out h_solo, unsigned long long *h_clamps, bool set_net,
+                       cudaStream_t st) {
+    (void)set_net;
+    void *stream = st;
+    const int64_t P = (int64_t)n_apps * (n_apps - 1) / 2;
+    const int nb = h_grid->n_budgets, G = h_grid->n_grid, S = h_grid->solo_offsets[nb];
+    const size_t n = (size_t)n_apps;
+#define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { \
+        fprintf(stderr, "cosched_b200: %s\n", cudaGetErrorString(_e)); return CS_ERR_CUDA; } } while (0)
+#define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
+    CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
+    CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     // queue counters and clamp counters are adjacent: one memset
     CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, (L.clamps - L.qcount) + sizeof(unsigned long long) * nb, st));
 
@@ -1434,7 +1537,6 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     dg.solo_knob = (const double *)(ws + L.solo_knob);
     cs_tables t;
     CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
-    if (fresh) CS_RC(cs_tables_set_network(net, &t, stream));
     cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
                    (int32_t *)(ws + L.solo_clamps)};
     CS_RC(cs_prepare(net, (const double *)(ws + L.feats), (const double *)(ws + L.bt), n_apps, &dg,
@@ -1457,10 +1559,11 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
     if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
     if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
-    CS_TRY(cudaStreamSynchronize(st));
 #undef CS_TRY
 #undef CS_RC
     return CS_OK;
 }
+}  // namespace
+
 
 }  // extern "C"

@@ -216,3 +216,31 @@ def test_all_pairs_4096_bit_exact_against_oracle(weights, grid_kind):
         assert np.array_equal(res.corun_time[0, b:e], ref["corun_time"][0])
         assert np.array_equal(res.weight[0, b:e], ref["weight"][0])
     assert res.screen_error < 2.5e-6
+
+
+def test_host_abi_repeated_calls_replay_a_graph_with_fresh_inputs(weights):
+    """cs_build_graph_host: the 3rd+ identical call replays a captured CUDA graph;
+    new input values in the same pinned buffers must still produce the oracle's
+    graph, and a changed network must invalidate the cached graph."""
+    from paper_2405_03831_b200.host_abi import HostGraphCall
+    spaces = [core.default_space(400.0)]
+    grid = KnobGrid(spaces)
+    n = 96
+    call = HostGraphCall(weights, grid, n)
+    for seed in (0, 1, 2, 3, 4):
+        F, T = workload(n, seed)
+        out = call(F, T)
+        ref = oracle.sweep(weights, F, T, grid)
+        iu, ju = np.triu_indices(n, 1)
+        assert np.array_equal(out["weights"][0][iu, ju], ref["weight"][0])
+        assert np.array_equal(out["corun_grid_index"][0], ref["corun_grid_index"][0])
+    # a different network on the same workspace and buffers
+    w2 = fnn.NetworkWeights(weights.w1 * 1.01, weights.b1, weights.w2, weights.b2, weights.w_out,
+                            weights.b_out, weights.feature_bounds)
+    from paper_2405_03831_b200.device import NetworkABI
+    call.net = NetworkABI(w2)
+    F, T = workload(n, 7)
+    out = call(F, T)
+    ref = oracle.sweep(w2, F, T, grid)
+    iu, ju = np.triu_indices(n, 1)
+    assert np.array_equal(out["weights"][0][iu, ju], ref["weight"][0])
