@@ -440,14 +440,22 @@ def run_ours(args):
         inp = scheduler.SchedulerInput(tuple(jobs), sp1[-1], _core.SchedulingParams(window=n1),
                                        weights)
         if n1 <= 4096:
-            scheduler.build_graph(inp)            # warm (plan cache, GPU path)
-            t0 = time.perf_counter()
-            graph = scheduler.build_graph(inp)
-            t1 = time.perf_counter()
-            matched = matcher.min_weight_perfect_matching(graph)
-            t2 = time.perf_counter()
-            scheduler.emit_schedule(inp, graph, matched)
-            t3 = time.perf_counter()
+            # HardwareConfig validates caps against the module constants
+            # (core.py:121-128 in the reference): a non-default cap grid needs
+            # them patched, exactly as the reference's own oracle run does
+            saved = (_core.CPU_CAPS, _core.GPU_CAPS)
+            _core.CPU_CAPS, _core.GPU_CAPS = sp1[-1].cpu_caps, sp1[-1].gpu_caps
+            try:
+                scheduler.build_graph(inp)            # warm (plan cache, GPU path)
+                t0 = time.perf_counter()
+                graph = scheduler.build_graph(inp)
+                t1 = time.perf_counter()
+                matched = matcher.min_weight_perfect_matching(graph)
+                t2 = time.perf_counter()
+                scheduler.emit_schedule(inp, graph, matched)
+                t3 = time.perf_counter()
+            finally:
+                _core.CPU_CAPS, _core.GPU_CAPS = saved
             result["schedule_e2e_s"] = {"total": t3 - t0, "build_graph": t1 - t0,
                                         "matching": t2 - t1, "emit": t3 - t2, "n_apps": n1}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
@@ -471,7 +479,8 @@ def main():
                              "tcgen05_v4_g4s2"] + [f"tcgen05_v4_g{g}s{s}_f{v}" for g, s in
                                                    ((3, 3), (4, 2)) for v in range(4)]
                     + ["tcgen05_v4_g4s2_f5", "tcgen05_v4_g3s3_f5", "tcgen05_v4_g4s2_f11",
-                       "tcgen05_v4_g4s2_f19", "tcgen05_v4_g2s4_f3"],
+                       "tcgen05_v4_g4s2_f19", "tcgen05_v4_g2s4_f3", "tcgen05_v4_g4s2_f35",
+                       "tcgen05_v4_g4s2_f37", "tcgen05_v4_g3s3_f35"],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -854,13 +854,14 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
             kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
             return CS_OK;
         };
-        const int V = (kind >> 12) & 0x1F;
+        const int V = (kind >> 12) & 0x3F;
 #define CS_TC3(GG, SS, VV) \
         if (G == GG && S == SS && V == VV) \
             return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
         CS_TC3(3, 3, 0) CS_TC3(3, 3, 1) CS_TC3(3, 3, 2) CS_TC3(3, 3, 3)
         CS_TC3(4, 2, 0) CS_TC3(4, 2, 1) CS_TC3(4, 2, 2) CS_TC3(4, 2, 3)
         CS_TC3(4, 2, 5) CS_TC3(3, 3, 5) CS_TC3(4, 2, 11) CS_TC3(4, 2, 19) CS_TC3(2, 4, 3)
+        CS_TC3(4, 2, 35) CS_TC3(4, 2, 37) CS_TC3(3, 3, 35)
 #undef CS_TC3
         return CS_ERR_ARG;
     }

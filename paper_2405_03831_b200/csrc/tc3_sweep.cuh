@@ -34,6 +34,9 @@ struct Cfg {
     static constexpr bool kComputeIssue = (V & 4) != 0;
     static constexpr bool kIssuerSpin = (V & 8) != 0;   // issuer polls instead of sleeping
     static constexpr bool kNoTensor = (V & 16) != 0;    // TIMING PROBE ONLY: no MMAs, no waits
+    // bit 5: read D(c) into registers, then build A(c+S) into the freed stage
+    // BEFORE the epilogue math of c -- MMA(c+S) is issued one epilogue earlier
+    static constexpr bool kEarlyIssue = (V & 32) != 0;
     static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
     static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
@@ -309,11 +312,13 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; bcl[l] = 0; }
 
             // epilogue of config c from stage s (s compile-time after unrolling)
-            auto epilogue = [&](int c, int s) {
-                if (!C::kNoTensor) tc3::mbar_wait_warp(&dr[s], ph[s]);
-                ph[s] ^= 1u;
-                tc::fence_after();
-                const float y = tc3::head_from_tmem(td[s], wo2, bo);
+            auto math = [&](int c, const float (&z)[HD]) {
+                float2 y2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int o = 0; o < 9; ++o)
+                    y2 = tc2::fma2(make_float2(fmaxf(z[2 * o], 0.f), fmaxf(z[2 * o + 1], 0.f)),
+                                   wo2[o], y2);
+                const float y = (y2.x + y2.y) + bo;
                 const int cl = y < 0.5f;
                 const float tm = fmaxf(y, 0.5f) * T_self;
                 const float tt = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
@@ -326,6 +331,17 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                         else second[l] = fminf(second[l], tt);
                     }
                 }
+            };
+            auto load_d = [&](int s, float (&z)[HD]) {
+                if (!C::kNoTensor) tc3::mbar_wait_warp(&dr[s], ph[s]);
+                ph[s] ^= 1u;
+                tc::fence_after();
+                tc::tmem_ld18(td[s], z);
+            };
+            auto epilogue = [&](int c, int s) {
+                float z[HD];
+                load_d(s, z);
+                math(c, z);
             };
             auto build = [&](int c, int s) {
                 tc3::build_row(p2, krow + (uint32_t)c * (2 * ROW32 * 4), ta[s]);
@@ -348,6 +364,27 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 asm volatile("" ::: "memory");   // keep build / epilogue phases apart
             };
 
+            if (C::kEarlyIssue) {
+                // pipeline: build(0 .. S-1); per c: D(c) -> registers, build(c+S)
+                // into the freed stage, then the math of c
+                auto step = [&](int cc, int s) {
+                    float z[HD];
+                    load_d(s, z);
+                    if (cc + S < n_cfg) build(cc + S, s);
+                    math(cc, z);
+                };
+#pragma unroll
+                for (int u = 0; u < S; ++u)
+                    if (u < n_cfg) build(u, u);
+                int c0 = 0;                              // c0 % S == 0 throughout
+                for (; c0 + S <= n_cfg; c0 += S) {
+#pragma unroll
+                    for (int u = 0; u < S; ++u) step(c0 + u, u);
+                }
+#pragma unroll
+                for (int u = 0; u < S; ++u)
+                    if (c0 + u < n_cfg) step(c0 + u, u);
+            } else {
             // software pipeline, stage of config c = c % S:
             //   build(0 .. S-2); [build(c), epilogue(c-S+1)] for c >= S-1; drain
 #pragma unroll
@@ -366,6 +403,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 const int cc = c + u, x = cc - (S - 1);
                 if (cc < n_cfg) build(cc, (S - 1 + u) % S);
                 if (x >= 0 && x < n_cfg) epilogue(x, u % S);
+            }
             }
 #pragma unroll
             for (int l = 0; l < L; ++l) clamps[l] += live ? bcl[l] : 0;

@@ -129,7 +129,8 @@ class SweepPlan:
                  # + flags: 0x1000 elected a_ready arrive, 0x2000 per-group issuer warps
                  **{f"tcgen05_v4_g{g}s{s}_f{v}": 0x300 | (g << 4) | s | (v << 12)
                     for g, s, v in [(3, 3, v) for v in range(4)] + [(4, 2, v) for v in range(4)]
-                    + [(4, 2, 5), (3, 3, 5), (4, 2, 11), (4, 2, 19), (2, 4, 3)]}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
+                    + [(4, 2, 5), (3, 3, 5), (4, 2, 11), (4, 2, 19), (2, 4, 3), (4, 2, 35),
+                       (4, 2, 37), (3, 3, 35)]}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
