@@ -159,12 +159,26 @@ def brute_force_matching(graph: PairGraph):
 
 
 def graph_to_csv(graph: PairGraph, path) -> None:
-    """One row per edge: i, j, repr(weight), co-run flag (matcher.py:132-142)."""
+    """One row per edge: i, j, repr(weight), co-run flag (matcher.py:132-142).
+
+    For a graph from the GPU sweep the flags come straight from the result
+    arrays (no per-edge PairDecision objects: 8.4M of them at N=4,096)."""
     n = graph.n
     dec = graph.decisions
+    flags_fn = getattr(dec, "corun_flags", None)
     with open(path, "w", newline="") as fh:
         out = csv.writer(fh)
         out.writerow(["i", "j", "weight", "corun_flag"])
+        if flags_fn is not None and len(dec) == n * (n - 1) // 2:
+            flags = flags_fn()
+            W = graph.weights
+            p = 0
+            for i in range(n):
+                row = W[i].tolist()
+                out.writerows([i, j, repr(row[j]), int(flags[p + (j - i - 1)])]
+                              for j in range(i + 1, n))
+                p += n - i - 1
+            return
         for i in range(n):
             for j in range(i + 1, n):
                 flag = ""

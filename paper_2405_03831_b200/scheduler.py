@@ -62,6 +62,10 @@ class PairDecisions(Mapping):
     def __len__(self) -> int:
         return self._n * (self._n - 1) // 2
 
+    def corun_flags(self) -> np.ndarray:
+        """corun_chosen of every pair, row-major i < j (no PairDecision objects)."""
+        return np.asarray(self._r.corun_chosen[self._l], dtype=bool)
+
     def potentials(self) -> np.ndarray:
         """Per-app best solo times: every pair weight is min(co-run, solo_i +
         solo_j) <= pot_i + pot_j, which the native matcher uses to solve the

@@ -106,3 +106,17 @@ def test_scalar_predictions_match_sweep(weights):
     assert abs(t - d.corun_time_s) <= REL * t
     total, splits = cs.solorun_time(weights, core.JobSet((jobs[2], jobs[5])), space)
     assert abs(total - d.solo_time_s) <= REL * total
+
+
+def test_graph_csv_fast_path_matches_generic(tmp_path, weights):
+    """graph_to_csv on a sweep graph (flag arrays, no PairDecision objects) writes
+    exactly what the generic per-edge path writes (matcher.py:132-142)."""
+    jobs = synth.generate_workload(2, synth.mixed_archetypes(40))
+    inp = cs.SchedulerInput(tuple(jobs), core.default_space(400.0),
+                            core.SchedulingParams(window=40), weights)
+    g = cs.build_graph(inp)
+    fast, slow = tmp_path / "fast.csv", tmp_path / "slow.csv"
+    cs.matcher.graph_to_csv(g, fast)
+    plain = cs.PairGraph(g.weights, {k: g.decisions[k] for k in g.decisions})
+    cs.matcher.graph_to_csv(plain, slow)
+    assert fast.read_text() == slow.read_text()
