@@ -249,6 +249,20 @@ int cs_packed_records_layout(void *d_base, int64_t cap, int32_t n_budgets, cs_pa
 int cs_scatter_gathered(const void *d_gathered, int32_t world, size_t rec_bytes, int64_t n_pairs,
                         int32_t n_apps, int32_t n_budgets, double *d_w, void *stream);
 
+/* The pair sweep with the reference's ANALYTIC oracle as the model
+ * (simenv.py:154-233) instead of the FNN.  The caller
+ * passes, config-major (G x N), the products resource*power of every app for
+ * the member-1 view (d_rp1) and the reversed-partition view (d_rp2), the apps'
+ * compute / memory intensities, coef = {compute_compute, memory_memory,
+ * compute_memory}, and the solo times (L x N).  Outputs as cs_pair_out
+ * (exact: fp64 without contraction); d_w (L x N x N, zeroed) optional;
+ * d_clamps (L, zeroed) counts co-run floor clamps. */
+int cs_analytic_sweep(const double *d_rp1, const double *d_rp2, const double *d_compute,
+                      const double *d_memory, const double *coef, const double *d_base_time,
+                      const double *d_solo_time, const uint32_t *d_mask, int32_t n_apps,
+                      int32_t n_grid, int32_t n_budgets, cs_pair_out out, double *d_w,
+                      unsigned long long *d_clamps, void *stream);
+
 /* fnn.forward_batch on rows x 40 normalized inputs (fp64, unfloored). */
 int cs_forward_rows(const cs_network *net, const double *d_x, int64_t rows, double *d_y,
                     void *stream);

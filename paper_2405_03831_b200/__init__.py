@@ -23,6 +23,7 @@ from .scheduler import (SchedulerInput, build_graph, predicted_makespan, schedul
                         schedule_to_json, set_time)
 from .synth import generate_workload, mixed_archetypes
 from .grid import KnobGrid
+from .analytic import OracleParams, OracleSlowdownModel, oracle_slowdown
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 

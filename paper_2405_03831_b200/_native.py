@@ -135,6 +135,11 @@ SWEEP_SYMBOLS = {
     "cs_scatter_gathered": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t,
                                            ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_analytic_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, c_double_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_int32, CsPairOut,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_forward_rows": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_void_p]),
     "cs_device_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),

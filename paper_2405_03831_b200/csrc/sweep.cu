@@ -742,6 +742,86 @@ __global__ void k_scatter_gathered(const uint8_t *__restrict__ gathered, int wor
     }
 }
 
+// ---- k_analytic: the simenv analytic oracle as the model (analytic.py) ----
+// Per pair, per config: slowdown_k = (resource*power)[view k][config][self] *
+// contention(self, other) (simenv.py:182-218, host-built products), floor
+// 0.5, x base time, max over members, per-budget first-index argmin, then the
+// co-run / time-share decision and the scatter.  fp64 with explicit _rn
+// intrinsics: no FMA contraction, so every value equals the reference's.
+struct AnalyticArgs {
+    const double *rp1, *rp2;        // G x N, config-major
+    const double *compute, *memory; // N
+    double cc, mm, cm;
+    const double *base_time, *solo_time;   // N ; L x N
+    const uint32_t *mask;           // G
+    int32_t n, G, L;
+    int64_t P;
+    cs_pair_out out;
+    double *W;
+    unsigned long long *clamps;
+};
+
+__device__ __forceinline__ double contention64(double cc, double mm, double cm, double ca, double ma,
+                                               double cb, double mb) {
+    // 1.0 + (cc*a.c*b.c + mm*a.m*b.m + cm*(a.c*b.m + a.m*b.c))   (simenv.py:175-179)
+    const double t1 = __dmul_rn(__dmul_rn(cc, ca), cb);
+    const double t2 = __dmul_rn(__dmul_rn(mm, ma), mb);
+    const double t3 = __dmul_rn(cm, __dadd_rn(__dmul_rn(ca, mb), __dmul_rn(ma, cb)));
+    return __dadd_rn(1.0, __dadd_rn(__dadd_rn(t1, t2), t3));
+}
+
+__global__ void __launch_bounds__(256) k_analytic(const AnalyticArgs a) {
+    unsigned long long cl[CS_MAX_BUDGETS] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < a.P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int i, j;
+        pair_of(p, a.n, i, j);
+        const double ci = a.compute[i], mi = a.memory[i], cj = a.compute[j], mj = a.memory[j];
+        const double c12 = contention64(a.cc, a.mm, a.cm, ci, mi, cj, mj);
+        const double c21 = contention64(a.cc, a.mm, a.cm, cj, mj, ci, mi);
+        const double Ti = a.base_time[i], Tj = a.base_time[j];
+        double best[CS_MAX_BUDGETS];
+        int idx[CS_MAX_BUDGETS];
+        for (int l = 0; l < CS_MAX_BUDGETS; ++l) { best[l] = INFINITY; idx[l] = -1; }
+        for (int c = 0; c < a.G; ++c) {
+            double s1 = __dmul_rn(a.rp1[(size_t)c * a.n + i], c12);
+            double s2 = __dmul_rn(a.rp2[(size_t)c * a.n + j], c21);
+            const int k1 = s1 < FLOOR, k2 = s2 < FLOOR;
+            s1 = k1 ? FLOOR : s1;
+            s2 = k2 ? FLOOR : s2;
+            const double t1 = __dmul_rn(s1, Ti), t2 = __dmul_rn(s2, Tj);
+            const double tt = t1 >= t2 ? t1 : t2;                 // max([t1, t2])
+            const uint32_t m = a.mask[c];
+            for (int l = 0; l < a.L; ++l)
+                if ((m >> l) & 1u) {
+                    cl[l] += k1 + k2;
+                    if (tt < best[l]) { best[l] = tt; idx[l] = c; }   // hwopt.py:59
+                }
+        }
+        for (int l = 0; l < a.L; ++l) {
+            const int64_t o = (int64_t)l * a.P + p;
+            const double *st = a.solo_time + (size_t)l * a.n;
+            const double solo = (0.0 + st[i]) + st[j];
+            const bool chosen = idx[l] >= 0 && best[l] <= solo;
+            const double w = chosen ? best[l] : solo;
+            a.out.corun_grid_index[o] = idx[l];
+            a.out.corun_time[o] = best[l];
+            a.out.corun_chosen[o] = chosen;
+            a.out.weight[o] = w;
+            if (a.W) {
+                double *Wl = a.W + (size_t)l * a.n * a.n;
+                Wl[(size_t)i * a.n + j] = w;
+                Wl[(size_t)j * a.n + i] = w;
+            }
+        }
+    }
+    for (int l = 0; l < a.L; ++l) {
+        unsigned long long v = cl[l];
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.clamps + l, v);
+    }
+}
+
 // ---- k_forward_rows: fnn.forward_batch, fp64 (fnn.py:161-165) -------------
 __global__ void k_forward_rows(const __grid_constant__ Net64P net, const double *__restrict__ x,
                                int64_t rows, double *__restrict__ y) {
@@ -1293,6 +1373,28 @@ int cs_scatter_gathered(const void *d_gathered, int32_t world, size_t rec_bytes,
     if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
     k_scatter_gathered<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
         (const uint8_t *)d_gathered, world, (int64_t)rec_bytes, n_pairs, n_apps, n_budgets, d_w);
+    return check_launch();
+}
+
+int cs_analytic_sweep(const double *d_rp1, const double *d_rp2, const double *d_compute,
+                      const double *d_memory, const double *coef, const double *d_base_time,
+                      const double *d_solo_time, const uint32_t *d_mask, int32_t n_apps,
+                      int32_t n_grid, int32_t n_budgets, cs_pair_out out, double *d_w,
+                      unsigned long long *d_clamps, void *stream) {
+    if (!d_rp1 || !d_rp2 || !d_compute || !d_memory || !coef || !d_base_time || !d_solo_time ||
+        !d_mask || n_apps < 2 || n_grid < 1 || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS ||
+        !out.corun_grid_index || !out.corun_time || !out.corun_chosen || !out.weight || !d_clamps)
+        return CS_ERR_ARG;
+    AnalyticArgs a{};
+    a.rp1 = d_rp1; a.rp2 = d_rp2; a.compute = d_compute; a.memory = d_memory;
+    a.cc = coef[0]; a.mm = coef[1]; a.cm = coef[2];
+    a.base_time = d_base_time; a.solo_time = d_solo_time; a.mask = d_mask;
+    a.n = n_apps; a.G = n_grid; a.L = n_budgets;
+    a.P = (int64_t)n_apps * (n_apps - 1) / 2;
+    a.out = out; a.W = d_w; a.clamps = d_clamps;
+    int64_t blocks = (a.P + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
+    k_analytic<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a);
     return check_launch();
 }
 

@@ -19,7 +19,7 @@ from typing import Sequence
 
 import numpy as np
 
-from . import estimator
+from . import analytic, estimator
 from .core import ConfigSpace, HardwareConfig, JobSet, Schedule, SchedulingParams, ValidationError, solo_config
 from .hwopt import PairDecision, decide_pair
 from .matcher import PairGraph, min_weight_perfect_matching
@@ -122,11 +122,18 @@ def build_graph(inp: SchedulerInput, jobs: int = 1) -> PairGraph:
     """Optimize every unordered pair and assemble the weighted pair graph.
 
     ``jobs`` keeps the reference's meaning (worker threads) for plugin models;
-    the FNN path is one GPU sweep regardless.
+    a trained network and the analytic oracle (``simenv.OracleSlowdownModel``)
+    are one GPU sweep regardless.
     """
     weights = estimator.fnn_weights_of(inp.model)
     if weights is not None:
         return build_graph_gpu(inp.queue, inp.space, weights)
+    oracle_params = analytic.oracle_params_of(inp.model)
+    if oracle_params is not None:
+        # the analytic oracle (simenv.OracleSlowdownModel): one exact GPU sweep
+        res = analytic.analytic_sweep(oracle_params, inp.queue, inp.space)
+        estimator.clamp_stats.count += int(res.clamps[0])
+        return PairGraph.trusted(res.matrix[0], PairDecisions(res, 0))
     n = len(inp.queue)
     pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
 

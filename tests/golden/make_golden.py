@@ -310,11 +310,56 @@ def stage_matching():
         json.dump(doc, fh)
 
 
+def stage_analytic():
+    """The analytic oracle (simenv.OracleSlowdownModel, simenv.py:221-233) as the
+    model of build_graph (scheduler.py:52-78): full graphs at N=24 (400 / 350 W,
+    default params and a perturbed set) and the reference schedule, plus
+    seeded decide_pair samples at N=512 on the five-budget levels."""
+    doc = {"graphs": [], "samples": []}
+    param_sets = {"default": simenv.OracleParams(),
+                  "perturbed": simenv.OracleParams(cpu_scaling=0.5, gpu_mem_scaling=0.8,
+                                                   compute_compute=0.4, memory_memory=0.1,
+                                                   compute_memory=0.2, cpu_power_penalty=0.7)}
+    for pname, params in param_sets.items():
+        model = simenv.OracleSlowdownModel(params)
+        for budget in (400.0, 350.0):
+            n = 24
+            jobs = jobs_for(n, 3)
+            space = core.default_space(budget)
+            inp = scheduler.SchedulerInput(tuple(jobs), space, core.SchedulingParams(window=n), model)
+            estimator.clamp_stats.reset()
+            g = scheduler.build_graph(inp)
+            sched = scheduler.schedule(inp)
+            doc["graphs"].append({
+                "params": pname, "params_json": params.to_json(), "n": n, "seed": 3,
+                "budget": budget,
+                "pairs": [_decision_row(space, i, j, g.decisions[(i, j)])
+                          for i in range(n) for j in range(i + 1, n)],
+                "schedule_sets": [[job.job_id for job in js.jobs] for js in sched.job_sets],
+                "schedule_flags": [bool(f) for f in sched.corun_flags],
+            })
+    rng = np.random.default_rng(99)
+    n = 512
+    jobs = jobs_for(n, 0)
+    model = simenv.OracleSlowdownModel(simenv.OracleParams())
+    for p_total in (325.0, 400.0):
+        space = core.ConfigSpace(p_total=p_total, cap_sum_levels=BUDGET_LEVELS)
+        rows = []
+        for _ in range(150):
+            i, j = sorted(rng.choice(n, size=2, replace=False).tolist())
+            rows.append(_decision_row(space, i, j, hwopt.decide_pair(model, jobs[i], jobs[j], space)))
+        doc["samples"].append({"n": n, "seed": 0, "p_total": p_total,
+                               "cap_sum_levels": list(BUDGET_LEVELS), "pairs": rows})
+    with open(os.path.join(HERE, "analytic.json"), "w") as fh:
+        json.dump(doc, fh, indent=0, sort_keys=True)
+
+
 STAGES = {
     "weights": stage_weights,
     "workloads": stage_workloads,
     "paper20": stage_paper20,
     "matching": stage_matching,
+    "analytic": stage_analytic,
     "samples": stage_samples,
     "n256": stage_n256,
 }
