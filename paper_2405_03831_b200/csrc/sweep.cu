@@ -611,8 +611,10 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
     __shared__ Head64P net_sm;
     __shared__ double red_v[4];
     __shared__ int red_i[4];
-    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
+    // blocks past the (device-side) queue length leave before staging anything
     const uint32_t count = *a.qcount;
+    if (blockIdx.x >= count) return;
+    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t q = blockIdx.x; q < count; q += gridDim.x) {
         const int64_t e = a.queue[q];
