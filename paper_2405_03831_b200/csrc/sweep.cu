@@ -381,6 +381,9 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
                                                 const double *__restrict__ base_time,
                                                 cs_solo_out solo, int do_solo) {
     __shared__ TablesSmem sm;
+    // let a programmatically dependent sweep start its prologue now (it still
+    // waits for this grid to finish before reading the tables)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     {
         // coalesced copy of the device image (Net64P | w1t): the parameter
         // bank would serialize these lane-divergent reads
@@ -933,7 +936,23 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
                 return CS_ERR_CUDA;
             int64_t c = (nblocks + groups - 1) / groups;
             if (c > sm_count()) c = sm_count();
-            kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
+            // programmatic dependent launch: the CTAs' prologue (TMEM allocation,
+            // mbarrier init) overlaps the tail of k_tables; the kernel waits on
+            // griddepcontrol.wait before it reads anything k_tables wrote
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)c);
+            cfg.blockDim = dim3((unsigned)threads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, kern, a, net, h64) != cudaSuccess) {
+                cudaGetLastError();
+                kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
+            }
             return CS_OK;
         };
         const int V = (kind >> 12) & 0x3F;

@@ -199,6 +199,17 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     const int warp = tid >> 5;
     const int lane = tid & 31;
 
+    // prologue that reads nothing of k_tables' output: barriers + TMEM first
+    if (tid == 0) {
+        for (int i = 0; i < G * S; ++i) {
+            tc::mbar_init(&d_ready[i], 1);
+            tc::mbar_init(&a_ready[i], C::kElected ? tc::kGroupThreads / 32 : tc::kGroupThreads);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+    // programmatic dependent launch: wait for k_tables' results to be visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int i = tid; i < tc2::kBBytes / 16; i += kThreads)
         reinterpret_cast<uint4 *>(b_tile)[i] =
             reinterpret_cast<const uint4 *>(a.t.w2_tile + tc::kBBytes / 2)[i];
@@ -211,14 +222,6 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     if (tid <= HD) wo_s[tid] = tid < HD ? net.wo[tid] : net.bo;
     for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += kThreads)
         reinterpret_cast<double *>(net64)[i] = __ldg(a.t.net_image + kImgHeadOff + i);
-    if (tid == 0) {
-        for (int i = 0; i < G * S; ++i) {
-            tc::mbar_init(&d_ready[i], 1);
-            tc::mbar_init(&a_ready[i], C::kElected ? tc::kGroupThreads / 32 : tc::kGroupThreads);
-        }
-        tc::fence_mbar_init();
-    }
-    if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
