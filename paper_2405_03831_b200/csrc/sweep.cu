@@ -344,6 +344,7 @@ struct TablesSmem {
     Net64P net;
     double w1t[IN][HD];
     Head64P head;
+    double xs[4][2 * NF];        // per warp: the app's normalized counters
 };
 
 // Best split of budget l for this warp's app from the splits evaluated by
@@ -407,14 +408,22 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
     for (int64_t r = tid >> 5; r < rows; r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         if (r < n) {
             const double f = lane < NF ? feats[r * NF + lane] : 0.0;
-            const double x1 = lane < NF ? clip01(f / net.bounds[lane]) : 0.0;
-            const double x2 = lane < NF ? clip01(f / net.bounds[NF + lane]) : 0.0;
+            // normalized counters through shared memory: the FMA chains below
+            // then read them with independent broadcast loads instead of a
+            // latency-bound shuffle per step
+            double *xs = sm.xs[threadIdx.x >> 5];
+            if (lane < NF) {
+                xs[lane] = clip01(f / net.bounds[lane]);
+                xs[NF + lane] = clip01(f / net.bounds[NF + lane]);
+            }
+            __syncwarp();
             double sa = 0.0, sb = 0.0;
 #pragma unroll
             for (int k = 0; k < NF; ++k) {
-                sa = fma(__shfl_sync(0xffffffffu, x1, k), sm.w1t[4 + k][h], sa);
-                sb = fma(__shfl_sync(0xffffffffu, x2, k), sm.w1t[4 + NF + k][h], sb);
+                sa = fma(xs[k], sm.w1t[4 + k][h], sa);
+                sb = fma(xs[NF + k], sm.w1t[4 + NF + k][h], sb);
             }
+            __syncwarp();
             if (lane < HD) {
                 t.app_a64[r * HD + h] = sa;
                 t.app_b64[r * HD + h] = sb;
