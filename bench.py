@@ -83,6 +83,16 @@ def measured_traffic(workload, kernel):
         return None
 
 
+def measured_issue(workload, kernel):
+    """Warp instructions per launch of the sweep kernel from the committed ncu
+    capture (profiles/issue.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as fh:
+            return json.load(fh).get(f"{workload}/{kernel}")
+    except (OSError, ValueError):
+        return None
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -225,6 +235,28 @@ def run_reference(args):
             "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def issue_roofline(args, kernel_ms, world):
+    """The binding roofline of the sweep kernel: CUDA-core instruction issue
+    (148 SMs x 4 schedulers x 1 warp-instruction/clock at the max SM clock).
+    Instructions per launch come from the committed ncu capture of the same
+    workload (1-GPU launch), so this is reported for world == 1 only."""
+    inst = measured_issue(args.workload, args.kernel)
+    if not inst or world != 1:
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mhz = json.load(fh).get("sm_max_mhz", 1965.0)
+    except (OSError, ValueError):
+        mhz = 1965.0
+    peak = sms * 4 * mhz * 1e6
+    achieved = inst / (kernel_ms / 1e3)
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-instr/s",
+            "frac": achieved / peak, "warp_instr_per_launch": inst,
+            "source": "smsp__inst_executed.sum of the ncu capture (profiles/issue.json)"}
 
 
 # --------------------------------------------------------------------------
@@ -378,6 +410,7 @@ def run_ours(args):
                          "flops_per_unit": FLOPS_PER_UNIT, "units_per_launch": units_local,
                          "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
                          "kernel_share_of_step": sweep_avg / (total_ms / args.steps)},
+            "roofline_issue": issue_roofline(args, sweep_avg, world),
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "screen": {"queue_len": c.queue_len, "max_rel_gap": c.screen_error},

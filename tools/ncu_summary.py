@@ -65,7 +65,7 @@ def _ncu(rep: str, *args) -> str:
 RAW_METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
-    ("sm__inst_executed.sum", "warp instructions executed"),
+    ("smsp__inst_executed.sum", "warp instructions executed"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy"),
     ("sm__inst_executed.sum.pct_of_peak_sustained_elapsed", "SM instruction throughput (of peak, elapsed)"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active"),
@@ -158,6 +158,14 @@ def main():
             d[a.traffic_key] = tot
             with open(path, "w") as fh:
                 json.dump(d, fh, indent=1, sort_keys=True)
+            # warp instructions executed by the captured launch (issue roofline)
+            inst = float(row[h.index("smsp__inst_executed.sum")]) if "smsp__inst_executed.sum" in h else None
+            if inst:
+                path = os.path.join(a.out, "issue.json")
+                d = json.load(open(path)) if os.path.exists(path) else {}
+                d[a.traffic_key] = inst
+                with open(path, "w") as fh:
+                    json.dump(d, fh, indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
