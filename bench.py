@@ -513,7 +513,8 @@ def main():
                                                    ((3, 3), (4, 2)) for v in range(4)]
                     + ["tcgen05_v4_g4s2_f5", "tcgen05_v4_g3s3_f5", "tcgen05_v4_g4s2_f11",
                        "tcgen05_v4_g4s2_f19", "tcgen05_v4_g2s4_f3", "tcgen05_v4_g4s2_f35",
-                       "tcgen05_v4_g4s2_f37", "tcgen05_v4_g3s3_f35"],
+                       "tcgen05_v4_g4s2_f37", "tcgen05_v4_g3s3_f35", "tcgen05_v5_g3s3",
+                       "tcgen05_v5_g3s2", "tcgen05_v5_g2s4", "tcgen05_v5_g2s3"],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -332,6 +332,7 @@ __device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&
 #include "tc_sweep.cuh"
 #include "tc2_sweep.cuh"
 #include "tc3_sweep.cuh"
+#include "tc4_sweep.cuh"
 
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -931,6 +932,26 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
         k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, h64);
         return CS_OK;
     }
+    if ((kind & 0xF00) == 0x400) {
+        // v5 warp-specialized screen (tc4_sweep.cuh): 0x4GS
+        const int G = (kind >> 4) & 0xF, S = kind & 0xF;
+        const size_t smem = tc4_smem_bytes(a.g.G);
+        if (smem > 227 * 1024) return CS_ERR_ARG;
+        auto go4 = [&](auto kern, int groups, int threads) -> int {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
+                return CS_ERR_CUDA;
+            int64_t c = (nblocks + groups - 1) / groups;
+            if (c > sm_count()) c = sm_count();
+            kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
+            return CS_OK;
+        };
+#define CS_TC4(GG, SS) \
+        if (G == GG && S == SS) return go4(k_sweep_tc4<L, GG, SS>, GG, tc4::Cfg<GG, SS>::kThreads);
+        CS_TC4(3, 3) CS_TC4(3, 2) CS_TC4(2, 4) CS_TC4(2, 3)
+#undef CS_TC4
+        return CS_ERR_ARG;
+    }
     if (kind == CS_KERNEL_TCGEN05 || (kind & 0xF00) == 0x300) {
         // v4 screen (tc3_sweep.cuh); 0xV3GS kinds select a (groups, stages,
         // variant flags) instance for tuning
@@ -1154,7 +1175,9 @@ int cs_pair_screen_fused(const cs_network *net, const cs_tables *tables, const c
                          int kernel_kind, void *stream) {
     if (!d_solo_time || !out.corun_chosen || !out.weight || !d_queue) return CS_ERR_ARG;
     if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
-    if (kernel_kind != CS_KERNEL_TCGEN05 && (kernel_kind & 0xF00) != 0x300) return CS_ERR_ARG;
+    if (kernel_kind != CS_KERNEL_TCGEN05 && (kernel_kind & 0xF00) != 0x300 &&
+        (kernel_kind & 0xF00) != 0x400)
+        return CS_ERR_ARG;
     return pair_screen_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
                             d_queue, d_queue_count, d_clamps, kernel_kind, d_solo_time,
                             d_solo_clamps, d_w, 1, stream);
@@ -1246,7 +1269,7 @@ int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_gr
     }
     if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
         kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100 &&
-        (kernel_kind & 0xF00) != 0x300)
+        (kernel_kind & 0xF00) != 0x300 && (kernel_kind & 0xF00) != 0x400)
         return CS_ERR_ARG;
     int lrc;
     switch (a.g.L) {

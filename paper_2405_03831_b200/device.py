@@ -130,7 +130,9 @@ class SweepPlan:
                  **{f"tcgen05_v4_g{g}s{s}_f{v}": 0x300 | (g << 4) | s | (v << 12)
                     for g, s, v in [(3, 3, v) for v in range(4)] + [(4, 2, v) for v in range(4)]
                     + [(4, 2, 5), (3, 3, 5), (4, 2, 11), (4, 2, 19), (2, 4, 3), (4, 2, 35),
-                       (4, 2, 37), (3, 3, 35)]}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
+                       (4, 2, 37), (3, 3, 35)]},
+                 # v5 warp-specialized screen (tc4_sweep.cuh)
+                 **{f"tcgen05_v5_g{g}s{s}": 0x400 | (g << 4) | s for g, s in ((3, 3), (3, 2), (2, 4), (2, 3))}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
@@ -194,7 +196,7 @@ class SweepPlan:
         # the v4 tcgen05 screen runs the fused pipeline: k_tables (+ solo
         # splits) -> k_sweep_tc3 (+ decide/scatter) -> k_resolve (+ decide);
         # the other screens keep tables | solo -> screen -> resolve -> decide
-        self.fused = kernel == "tcgen05" or kernel.startswith("tcgen05_v4")
+        self.fused = kernel == "tcgen05" or kernel.startswith(("tcgen05_v4", "tcgen05_v5"))
         self.launches_per_run = 3 if self.fused else 5
 
     # ------------------------------------------------------------------

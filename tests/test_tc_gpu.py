@@ -20,7 +20,7 @@ def _check(res, ref, L):
         assert np.array_equal(res.weight[l], ref["weight"][l])
 
 
-@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_v4_g4s2_f5", "tcgen05_v4_g4s2_f37", "tcgen05_v4_g3s3_f35", "tcgen05_v3", "tcgen05_smem", "simt",
+@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05_v4_g4s2_f5", "tcgen05_v4_g4s2_f37", "tcgen05_v4_g3s3_f35", "tcgen05_v5_g3s3", "tcgen05_v5_g2s4", "tcgen05_v3", "tcgen05_smem", "simt",
                                     "tcgen05_g2s4"])
 @pytest.mark.parametrize("n,seed,budgets", [
     (20, 0, (400.0,)), (2, 1, (400.0,)), (67, 2, (350.0,)), (131, 3, (400.0, 350.0)),
