@@ -308,10 +308,18 @@ def run_ours(args):
                 plan.launch(d_f, d_b)
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize(dev)
+        # two captures of the same step: with the kernel events (every
+        # --event-every'th timed step: the dominant kernel's own duration) and
+        # without (an event between two kernels costs the graph its launch
+        # overlap, a few us per boundary)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             plan.launch(d_f, d_b, (ev_s, ev_e))
+        graph_plain = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_plain):
+            plan.launch(d_f, d_b)
         step = graph.replay
+        step_plain = graph_plain.replay
         launches_per_step = plan.launches_per_run
         units_local = P * upp
     else:
@@ -325,6 +333,7 @@ def run_ours(args):
 
         def step():
             sh.run(d_f, d_b, (ev_s, ev_e))
+        step_plain = None
         graph_mode = "eager"
         if dist.get_backend() == "nccl" and not os.environ.get("COSCHED_NO_GRAPH"):
             # the whole step -- shard sweep, NCCL all-gather, device scatter -- as
@@ -340,6 +349,7 @@ def run_ours(args):
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
                 if int(ok) == 1:
                     step, graph_mode = g.replay, "cuda-graph (sweep + NCCL all-gather + scatter)"
+                    step_plain = None
             except Exception as exc:   # capture unsupported here: stay eager
                 print(f"rank {rank}: graph capture failed ({exc}); eager steps", file=sys.stderr)
                 torch.cuda.synchronize(dev)
@@ -360,14 +370,16 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     with ClockSampler(local_rank) as clk:
         t_wall = time.perf_counter()
-        for _ in range(args.steps):
+        for k in range(args.steps):
             flush.zero_()                       # L2 flush, outside the step events
+            sample = step_plain is None or k % args.event_every == 0
             st.record()
-            step()
+            (step if sample else step_plain)()
             en.record()
             en.synchronize()
             step_ms.append(st.elapsed_time(en))
-            sweep_ms.append(ev_s.elapsed_time(ev_e))
+            if sample:
+                sweep_ms.append(ev_s.elapsed_time(ev_e))
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t_wall
     if world > 1:
@@ -394,6 +406,8 @@ def run_ours(args):
             "config": {"workload": WORKLOADS[args.workload][3], "n_apps": n, "pairs": P,
                        "configs_per_pair": upp, "budgets": [s.p_total for s in spaces],
                        "l2": "flushed before every step (256 MiB memset, outside the events)",
+                       "kernel_events": (f"sweep kernel timed on every {args.event_every}th step "
+                                         "(same graph + 2 events)" if world == 1 else "every step"),
                        "step": ("CUDA graph: k_tables (+solo splits) -> k_sweep_tc3 (+decide, "
                                 "scatter) -> k_resolve (+decide)" if world == 1 else
                                 "shard sweep (3 kernels) -> ONE all-gather of the packed pair "
@@ -519,6 +533,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--event-every", type=int, default=16,
+                    help="time the dominant kernel with CUDA events on every k-th timed step "
+                         "(the other steps replay the same graph without the events)")
     ap.add_argument("--ref-budget-s", type=float, default=90.0,
                     help="total wall budget of the --impl reference run")
     args = ap.parse_args()
