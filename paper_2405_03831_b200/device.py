@@ -101,6 +101,17 @@ class SweepCounters:
     clamps: np.ndarray
 
 
+def fp16_screen_safe(weights) -> bool:
+    """Whether the tensor-core screen's fp16 operands can hold this network:
+    every layer-1 pre-activation |z1| and every |W2|, |b2| well inside the fp16
+    range (the same bound cs_pair_screen's CS_KERNEL_AUTO applies).  Inputs are
+    normalized to [0, 1], so |z1| <= |b1| + sum |W1| row-wise."""
+    w1 = np.abs(np.asarray(weights.w1, dtype=np.float64))
+    zmax = float(np.max(np.abs(np.asarray(weights.b1, dtype=np.float64)) + w1.sum(axis=1)))
+    wmax = float(max(np.max(np.abs(weights.w2)), np.max(np.abs(weights.b2))))
+    return zmax < 30000.0 and wmax < 30000.0
+
+
 class SweepPlan:
     """All device buffers for sweeping `n` apps over `grid`, pairs [begin, end)."""
 
@@ -135,6 +146,10 @@ class SweepPlan:
                  **{f"tcgen05_v5_g{g}s{s}": 0x400 | (g << 4) | s for g, s in ((3, 3), (3, 2), (2, 4), (2, 3))}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
+        if kernel == "tcgen05" and not fp16_screen_safe(weights):
+            # a network beyond the fp16 operand range takes the fp32 SIMT screen
+            # (identical results: the exact fp64 steps are shared)
+            kernel = "simt"
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
         self.pair_begin, self.pair_end = int(pair_begin), pair_end
         self.P = pair_end - pair_begin

@@ -49,3 +49,20 @@ def test_five_budgets_and_fine_grid_shards(weights, kernel):
                              gpu_caps=tuple(150.0 + 6.25 * k for k in range(17)), p_total=400.0)]
     res = sweep_pairs(weights, jobs, fine, b, e, with_matrix=False, kernel=kernel)
     _check(res, oracle.sweep(weights, F, T, KnobGrid(fine), b, e), 1)
+
+
+def test_out_of_fp16_range_network_falls_back_and_stays_exact(weights):
+    """A network whose layer-1 activations exceed the fp16 range cannot use the
+    tensor-core screen; the default plan must switch to the fp32 SIMT screen and
+    still match the oracle exactly."""
+    from paper_2405_03831_b200 import fnn
+    from paper_2405_03831_b200.device import fp16_screen_safe
+    big = fnn.NetworkWeights(weights.w1 * 5000.0, weights.b1 * 5000.0, weights.w2, weights.b2,
+                             weights.w_out, weights.b_out, weights.feature_bounds)
+    assert fp16_screen_safe(weights) and not fp16_screen_safe(big)
+    n = 48
+    jobs = synth.generate_workload(5, synth.mixed_archetypes(n))
+    spaces = [core.default_space(400.0)]
+    res = sweep_pairs(big, jobs, spaces, with_matrix=False)
+    F, T = workload(n, 5)
+    _check(res, oracle.sweep(big, F, T, KnobGrid(spaces)), 1)
