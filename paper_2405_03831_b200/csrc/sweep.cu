@@ -1193,11 +1193,40 @@ int cs_resolve_fused(const cs_network *net, const cs_tables *tables, const cs_gr
                         d_queue_count, d_solo_time, d_solo_clamps, d_clamps, d_w, 1, stream);
 }
 
+namespace {
+// the tensor-core screen's fp16 operands must hold |z1| and |W2|, |b2|
+bool fp16_screen_safe(const cs_network *net) {
+    Net64P n64;
+    if (!net64_from(net, &n64)) return false;
+    double zmax = 0.0, wmax = 0.0;
+    for (int h = 0; h < HD; ++h) {
+        double r = fabs(n64.b1[h]);
+        for (int k = 0; k < IN; ++k) r += fabs(n64.w1[h * IN + k]);
+        zmax = fmax(zmax, r);
+        wmax = fmax(wmax, fabs(n64.b2[h]));
+        for (int k = 0; k < HD; ++k) wmax = fmax(wmax, fabs(n64.w2[h * HD + k]));
+    }
+    return zmax < 30000.0 && wmax < 30000.0;
+}
+}  // namespace
+
 int cs_pair_sweep_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                         const double *d_base_time, const double *d_solo_time,
                         const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
                         double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
                         unsigned long long *d_clamps, double *d_w, int kernel_kind, void *stream) {
+    if (kernel_kind == CS_KERNEL_AUTO && !fp16_screen_safe(net)) {
+        // beyond the fp16 range: the fp32 SIMT screen, then resolve + decide
+        // (+ scatter) as separate steps -- identical results
+        int rc = cs_pair_screen(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps,
+                                out, d_queue, d_queue_count, d_clamps, CS_KERNEL_SIMT, stream);
+        if (rc) return rc;
+        rc = cs_resolve(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
+                        d_queue_count, stream);
+        if (rc) return rc;
+        return cs_pair_decide(d_grid, d_solo_time, d_solo_clamps, tables->n_apps, pair_begin,
+                              pair_end, out, d_clamps, d_w, stream);
+    }
     int rc = cs_pair_screen_fused(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
                                   pair_begin, pair_end, rel_eps, out, d_queue, d_queue_count,
                                   d_clamps, d_w, kernel_kind, stream);

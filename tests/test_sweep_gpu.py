@@ -244,3 +244,19 @@ def test_host_abi_repeated_calls_replay_a_graph_with_fresh_inputs(weights):
     ref = oracle.sweep(w2, F, T, grid)
     iu, ju = np.triu_indices(n, 1)
     assert np.array_equal(out["weights"][0][iu, ju], ref["weight"][0])
+
+
+def test_host_abi_out_of_fp16_range_network(weights):
+    """cs_build_graph_host (CS_KERNEL_AUTO) with a network beyond the fp16 range
+    takes the SIMT screen + resolve + decide path and matches the oracle."""
+    from paper_2405_03831_b200.host_abi import build_graph_host
+    big = fnn.NetworkWeights(weights.w1 * 5000.0, weights.b1 * 5000.0, weights.w2, weights.b2,
+                             weights.w_out, weights.b_out, weights.feature_bounds)
+    n = 40
+    grid = KnobGrid([core.default_space(400.0)])
+    F, T = workload(n, 6)
+    out = build_graph_host(big, grid, F, T)
+    ref = oracle.sweep(big, F, T, grid)
+    iu, ju = np.triu_indices(n, 1)
+    assert np.array_equal(out["weights"][0][iu, ju], ref["weight"][0])
+    assert np.array_equal(out["corun_grid_index"][0], ref["corun_grid_index"][0])
