@@ -57,7 +57,8 @@ enum {
     CS_ERR_NO_CONFIG = -2,    /* a budget admits no co-run config      (hwopt.py:62-64)   */
     CS_ERR_UNREACHABLE = -3,  /* a budget admits no solo split         (estimator.py:165) */
     CS_ERR_CUDA = -4,         /* CUDA launch/runtime failure           -> RuntimeError    */
-    CS_ERR_WORKSPACE = -5     /* workspace smaller than required       -> ValueError      */
+    CS_ERR_WORKSPACE = -5,    /* workspace smaller than required       -> ValueError      */
+    CS_ERR_PRECISION = -6     /* screen error beyond any usable rel_eps -> RuntimeError   */
 };
 
 /* Screen kernels of cs_pair_sweep_ex (results are identical: both feed the same

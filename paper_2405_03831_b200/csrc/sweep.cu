@@ -1033,6 +1033,7 @@ const char *cs_error_string(int code) {
         case CS_ERR_NO_CONFIG: return "no co-run configs exist for a requested budget";
         case CS_ERR_UNREACHABLE: return "budget is unreachable on the cap grids (no solo split)";
         case CS_ERR_CUDA: return "CUDA runtime error";
+        case CS_ERR_PRECISION: return "fp32 screen error too large for an exact argmin";
         case CS_ERR_WORKSPACE: return "workspace too small";
         default: return "unknown error";
     }
@@ -1553,7 +1554,7 @@ namespace {
 int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                        const double *h_base_time, int32_t n_apps, double rel_eps, char *ws,
                        const GraphLayout &L, double *h_weights, cs_pair_out h_pairs,
-                       cs_solo_out h_solo, unsigned long long *h_clamps, bool set_net,
+                       cs_solo_out h_solo, unsigned long long *h_clamps, uint32_t *h_counters,
                        cudaStream_t st);
 
 struct HostCallKey {
@@ -1612,13 +1613,20 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     }
     static std::mutex cache_mu;
     static std::unordered_map<const void *, std::vector<uint8_t>> cache;
+    // one pinned 2-word counter slot per workspace (read back inside the call
+    // and its graph; lives as long as the process)
+    static std::unordered_map<const void *, uint32_t *> counters;
     bool fresh;
+    uint32_t *h_counters = nullptr;
     {
         std::lock_guard<std::mutex> lock(cache_mu);
         auto it = cache.find(d_workspace);
         fresh = it == cache.end() || it->second != key;
         if (fresh) cache[d_workspace] = key;   // recorded before the upload: a failure below
-    }                                           // returns an error and the caller retries
+        uint32_t *&slot = counters[d_workspace];   // returns an error and the caller retries
+        if (!slot) CS_TRY(cudaHostAlloc((void **)&slot, sizeof(uint32_t) * 2, cudaHostAllocDefault));
+        h_counters = slot;
+    }
     if (fresh) {
         if (G) {
             CS_TRY(cudaMemcpyAsync(ws + L.knob1, h_grid->knob1, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
@@ -1672,7 +1680,7 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
         cudaGraphExec_t ge = nullptr;
         bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
         int erc = ok ? enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
-                                          h_weights, h_pairs, h_solo, h_clamps, false, st)
+                                          h_weights, h_pairs, h_solo, h_clamps, h_counters, st)
                      : CS_ERR_CUDA;
         if (ok) ok = cudaStreamEndCapture(st, &graph) == cudaSuccess && erc == CS_OK;
         if (ok) ok = cudaGraphInstantiate(&ge, graph, 0) == cudaSuccess;
@@ -1685,12 +1693,26 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
         }
         if (ok) CS_TRY(cudaGraphLaunch(ge, st));
         else CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
-                                      h_weights, h_pairs, h_solo, h_clamps, false, st));
+                                      h_weights, h_pairs, h_solo, h_clamps, h_counters, st));
     } else {
         CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
-                                 h_weights, h_pairs, h_solo, h_clamps, false, st));
+                                 h_weights, h_pairs, h_solo, h_clamps, h_counters, st));
     }
     CS_TRY(cudaStreamSynchronize(st));
+    // The screen's certain winners carry the observed fp32-vs-fp64 gap; argmin
+    // parity needs it well inside rel_eps.  Otherwise (a network far outside
+    // the trained range) redo the call with a wider ambiguity band -- more
+    // pairs go to the exact fp64 resolve, the results stay identical.
+    for (double eps = rel_eps;;) {
+        float err;
+        memcpy(&err, h_counters + 1, sizeof(err));
+        if (!(err > 0.25 * eps)) break;
+        eps = fmax(16.0 * eps, 16.0 * (double)err);
+        if (!(eps < 0.1)) return CS_ERR_PRECISION;
+        CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, eps, ws, L,
+                                 h_weights, h_pairs, h_solo, h_clamps, h_counters, st));
+        CS_TRY(cudaStreamSynchronize(st));
+    }
 #undef CS_TRY
 #undef CS_RC
     return CS_OK;
@@ -1700,9 +1722,8 @@ namespace {
 int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                        const double *h_base_time, int32_t n_apps, double rel_eps, char *ws,
                        const GraphLayout &L, double *h_weights, cs_pair_out h_pairs,
-                       cs_solo_out h_solo, unsigned long long *h_clamps, bool set_net,
+                       cs_solo_out h_solo, unsigned long long *h_clamps, uint32_t *h_counters,
                        cudaStream_t st) {
-    (void)set_net;
     void *stream = st;
     const int64_t P = (int64_t)n_apps * (n_apps - 1) / 2;
     const int nb = h_grid->n_budgets, G = h_grid->n_grid, S = h_grid->solo_offsets[nb];
@@ -1744,6 +1765,8 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
     if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
     if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
+    // queue length + screen-error monitor, checked by the caller after the sync
+    CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
 #undef CS_TRY
 #undef CS_RC
     return CS_OK;
