@@ -110,7 +110,7 @@ __device__ __forceinline__ void pair_of(int64_t p, int n, int &i, int &j) {
 // operands, no loads).  Loop order k-outer / o-inner keeps 18 independent
 // accumulation chains in flight while every chain still sums over k in the
 // oracle's order, so results stay bit-identical to it.
-struct Head64P {
+struct __align__(16) Head64P {   // 16 B: read with ld.shared.v2.f64
     double w2[HD * HD];
     double b2[HD];
     double wo[HD];
@@ -156,27 +156,48 @@ __device__ __forceinline__ double head64c(const Head64P &net_in, const double (&
 
 // Register-lean variant (three output units per pass) for kernels whose
 // per-thread work is a handful of heads (k_solo): same summation order.
+// Two fp64 weights from shared memory (16 B, broadcast across the warp).
+// Volatile so that the prefetches below stay where they are written:
+// ptxas otherwise sinks each load next to its use at high register pressure
+// and every DFMA then waits out a full LDS latency.
+__device__ __forceinline__ double2 lds_f64x2(const double *p) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
+// Layer 2 + head in fp64, the oracle's fma order (per output: k ascending,
+// then + b2; y: o ascending).  `net` MUST live in shared memory (every
+// caller stages it there).  Two output rows at a time, their weights
+// prefetched one double2 step ahead.
 __device__ __forceinline__ double head64_lean(const Head64P &net, const double (&z)[HD]) {
     double h1[HD];
 #pragma unroll
     for (int k = 0; k < HD; ++k) h1[k] = z[k] > 0.0 ? z[k] : 0.0;
     double y = 0.0;
 #pragma unroll 1
-    for (int o = 0; o < HD; o += 3) {
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-        const double *r0 = net.w2 + o * HD, *r1 = r0 + HD, *r2 = r1 + HD;
+    for (int o = 0; o < HD; o += 2) {
+        const double *r0 = net.w2 + o * HD, *r1 = r0 + HD;
+        double acc0 = 0.0, acc1 = 0.0;
+        double2 w0 = lds_f64x2(r0), w1 = lds_f64x2(r1);
 #pragma unroll
-        for (int k = 0; k < HD; ++k) {
-            acc0 = fma(h1[k], r0[k], acc0);
-            acc1 = fma(h1[k], r1[k], acc1);
-            acc2 = fma(h1[k], r2[k], acc2);
+        for (int k = 0; k < HD; k += 2) {
+            double2 n0 = w0, n1 = w1;
+            if (k + 2 < HD) { n0 = lds_f64x2(r0 + k + 2); n1 = lds_f64x2(r1 + k + 2); }
+            acc0 = fma(h1[k], w0.x, acc0);
+            acc1 = fma(h1[k], w1.x, acc1);
+            acc0 = fma(h1[k + 1], w0.y, acc0);
+            acc1 = fma(h1[k + 1], w1.y, acc1);
+            w0 = n0;
+            w1 = n1;
         }
-        acc0 = acc0 + net.b2[o];
-        acc1 = acc1 + net.b2[o + 1];
-        acc2 = acc2 + net.b2[o + 2];
-        y = fma(acc0 > 0.0 ? acc0 : 0.0, net.wo[o], y);
-        y = fma(acc1 > 0.0 ? acc1 : 0.0, net.wo[o + 1], y);
-        y = fma(acc2 > 0.0 ? acc2 : 0.0, net.wo[o + 2], y);
+        const double2 b = lds_f64x2(net.b2 + o), wo = lds_f64x2(net.wo + o);
+        acc0 = acc0 + b.x;
+        acc1 = acc1 + b.y;
+        y = fma(acc0 > 0.0 ? acc0 : 0.0, wo.x, y);
+        y = fma(acc1 > 0.0 ? acc1 : 0.0, wo.y, y);
     }
     y = y + net.bo;
     return y > 0.0 ? y : 0.0;
@@ -201,16 +222,41 @@ __device__ __forceinline__ const Head64P &stage_head64(const double *__restrict_
     return sm;
 }
 
+// The fp64 tables are chunk-major so that a warp's gather is coalesced: the
+// 18 values of a row are 9 double2 chunks, and chunk q of every row is
+// stored together.  App rows: [9][N] double2 -- lanes reading consecutive
+// apps (the j's of a pair block) hit consecutive 16 B.  Knob rows: [9][G][2]
+// double2, member 0 (K1) and member 1 (K2) of a config side by side;
+// knob2_64 = knob1_64 + 2, both indexed with member 0's index.
+__host__ __device__ __forceinline__ size_t app64_at(int n, int r, int h) {
+    return ((size_t)(h >> 1) * n + r) * 2 + (h & 1);
+}
+__host__ __device__ __forceinline__ size_t knob64_at(int G, int c, int member, int h) {
+    return (((size_t)(h >> 1) * G + c) * 2 + member) * 2 + (h & 1);
+}
+
+// z = (A_self + B_other) + K_c in fp64, the oracle's sum order (16 B loads)
+__device__ __forceinline__ void z64_row(const cs_tables &t, int self, int other, int c, int member,
+                                        double (&z)[HD]) {
+    const double2 *as = reinterpret_cast<const double2 *>(t.app_a64) + self;
+    const double2 *bo = reinterpret_cast<const double2 *>(t.app_b64) + other;
+    const double2 *kk = reinterpret_cast<const double2 *>(t.knob1_64) + 2 * (size_t)c + member;
+    const size_t sn = (size_t)t.n_apps, sg = 2 * (size_t)t.n_grid;
+#pragma unroll
+    for (int q = 0; q < HD / 2; ++q) {
+        const double2 a = __ldg(as + q * sn), b = __ldg(bo + q * sn), k = __ldg(kk + q * sg);
+        z[2 * q] = (a.x + b.x) + k.x;
+        z[2 * q + 1] = (a.y + b.y) + k.y;
+    }
+}
+
 // floor(pred) x T of one member of pair (self, other) under config c
 // (member 0: K1 / view hc, member 1: K2 / reversed partitions)
 __device__ __forceinline__ double member_time64(const cs_tables &t, const Head64P &net,
                                                 const double *__restrict__ base_time, int self,
                                                 int other, int c, int member) {
     double z[HD];
-    const double *as = t.app_a64 + (size_t)self * HD, *bo = t.app_b64 + (size_t)other * HD;
-    const double *kk = (member ? t.knob2_64 : t.knob1_64) + (size_t)c * HD;
-#pragma unroll
-    for (int h = 0; h < HD; ++h) z[h] = (__ldg(as + h) + __ldg(bo + h)) + __ldg(kk + h);
+    z64_row(t, self, other, c, member, z);
     const double y = head64c(net, z);
     return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
 }
@@ -219,10 +265,7 @@ __device__ __forceinline__ double member_time64_lean(const cs_tables &t, const H
                                                      const double *__restrict__ base_time,
                                                      int self, int other, int c, int member) {
     double z[HD];
-    const double *as = t.app_a64 + (size_t)self * HD, *bo = t.app_b64 + (size_t)other * HD;
-    const double *kk = (member ? t.knob2_64 : t.knob1_64) + (size_t)c * HD;
-#pragma unroll
-    for (int h = 0; h < HD; ++h) z[h] = (__ldg(as + h) + __ldg(bo + h)) + __ldg(kk + h);
+    z64_row(t, self, other, c, member, z);
     const double y = head64_lean(net, z);
     return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
 }
@@ -426,8 +469,8 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
             }
             __syncwarp();
             if (lane < HD) {
-                t.app_a64[r * HD + h] = sa;
-                t.app_b64[r * HD + h] = sb;
+                t.app_a64[app64_at(n, (int)r, h)] = sa;
+                t.app_b64[app64_at(n, (int)r, h)] = sb;
                 t.app_a32[r * ROW32 + h] = (float)sa;
                 t.app_b32[r * ROW32 + h] = (float)sb;
             } else if (lane < ROW32) {
@@ -465,8 +508,8 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
             s1 = s1 + net.b1[h];
             s2 = s2 + net.b1[h];
             if (lane < HD) {
-                t.knob1_64[c * HD + h] = s1;
-                t.knob2_64[c * HD + h] = s2;
+                t.knob1_64[knob64_at(g.G, (int)c, 0, h)] = s1;
+                t.knob1_64[knob64_at(g.G, (int)c, 1, h)] = s2;
                 t.knob1_32[c * ROW32 + h] = (float)s1;
                 t.knob2_32[c * ROW32 + h] = (float)s2;
             } else if (lane < ROW32) {
@@ -500,7 +543,7 @@ __global__ void k_solo(const cs_tables t, const GridP g, const double *__restric
     for (int s = lane; s < ns; s += 32) {
         double z[HD];
 #pragma unroll
-        for (int h = 0; h < HD; ++h) z[h] = t.app_a64[(size_t)a * HD + h] + t.solo64[(size_t)(s0 + s) * HD + h];
+        for (int h = 0; h < HD; ++h) z[h] = t.app_a64[app64_at(n, a, h)] + t.solo64[(size_t)(s0 + s) * HD + h];
         double y = head64_lean(net, z);
         if (y < FLOOR) { ++clamp; y = FLOOR; }
         const double tt = y * base_time[a];
@@ -985,7 +1028,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
             }
             return CS_OK;
         };
-        const int V = (kind >> 12) & 0x3F;
+        const int V = (kind >> 12) & 0xFF;
 #define CS_TC3(GG, SS, VV) \
         if (G == GG && S == SS && V == VV) \
             return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
@@ -993,6 +1036,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
         CS_TC3(4, 2, 0) CS_TC3(4, 2, 1) CS_TC3(4, 2, 2) CS_TC3(4, 2, 3)
         CS_TC3(4, 2, 5) CS_TC3(3, 3, 5) CS_TC3(4, 2, 11) CS_TC3(4, 2, 19) CS_TC3(2, 4, 3)
         CS_TC3(4, 2, 35) CS_TC3(4, 2, 37) CS_TC3(3, 3, 35)
+        CS_TC3(4, 2, 67) CS_TC3(4, 2, 131) CS_TC3(4, 2, 195)
 #undef CS_TC3
         return CS_ERR_ARG;
     }
@@ -1066,8 +1110,9 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
     out->app_b64 = (double *)take(sizeof(double) * (size_t)n_apps * HD);
     out->knob1_32 = (float *)take(sizeof(float) * (size_t)n_grid * ROW32);
     out->knob2_32 = (float *)take(sizeof(float) * (size_t)n_grid * ROW32);
-    out->knob1_64 = (double *)take(sizeof(double) * (size_t)n_grid * HD);
-    out->knob2_64 = (double *)take(sizeof(double) * (size_t)n_grid * HD);
+    // fp64 knob rows of both members interleaved per chunk (see knob64_at)
+    out->knob1_64 = (double *)take(2 * sizeof(double) * (size_t)n_grid * HD);
+    out->knob2_64 = out->knob1_64 + 2;
     out->solo64 = (double *)take(sizeof(double) * (size_t)n_solo * HD);
     out->net_image = (double *)take(sizeof(double) * (size_t)kImgDoubles);
     return CS_OK;

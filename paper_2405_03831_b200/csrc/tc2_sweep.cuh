@@ -167,10 +167,11 @@ __global__ void __launch_bounds__(Tc2Cfg<G, S>::kThreads, 1)
     // d_ready[g*S+s]: MMA -> epilogue (tcgen05.commit, count 1)
     // a_ready[g*S+s]: A rows in TMEM -> MMA issuer (one arrive per compute warp, count 4)
     uint64_t *d_ready = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
+        smem + ((reinterpret_cast<uint8_t *>(masks + a.g.G) - smem + 7) & ~ptrdiff_t(7)));
     uint64_t *a_ready = d_ready + G * S;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + G * S);
-    Head64P *net64 = reinterpret_cast<Head64P *>(a_ready + G * S + 2);
+    Head64P *net64 = reinterpret_cast<Head64P *>(
+        smem + ((reinterpret_cast<uint8_t *>(a_ready + G * S + 2) - smem + 15) & ~ptrdiff_t(15)));
 
     const int tid = threadIdx.x;
     const int g = tid / tc::kGroupThreads;     // >= G: the MMA-issuer warps
@@ -370,6 +371,6 @@ inline size_t tc2_smem_bytes(int n_grid) {
     size_t b = (size_t)tc2::kBBytes;
     b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * 16 * sizeof(uint64_t) + 16 + sizeof(Head64P);
+    b += 2 * 16 * sizeof(uint64_t) + 32 + sizeof(Head64P);
     return b;
 }

@@ -37,6 +37,10 @@ struct Cfg {
     // bit 5: read D(c) into registers, then build A(c+S) into the freed stage
     // BEFORE the epilogue math of c -- MMA(c+S) is issued one epilogue earlier
     static constexpr bool kEarlyIssue = (V & 32) != 0;
+    // TIMING PROBES ONLY (wrong results): bit 6 skips the fp64 winner
+    // re-evaluation, bit 7 skips the record / matrix writes of the tail
+    static constexpr bool kNoExact = (V & 64) != 0;
+    static constexpr bool kNoWrite = (V & 128) != 0;
     static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
     static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
@@ -161,6 +165,14 @@ __device__ __forceinline__ void build_row(const float2 (&p2)[9], uint32_t krow, 
     tc::fence_before();
 }
 
+__device__ __forceinline__ float2 lds_f32x2(const float *p) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+                 : "=f"(v.x), "=f"(v.y)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 // y = wo . ReLU(z2) + bo for this thread's row of one config (fp32, FFMA2)
 __device__ __forceinline__ float head_from_tmem(uint32_t taddr, const float2 (&wo2)[9], float bo) {
     float z[HD];
@@ -187,10 +199,11 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     float *k12 = reinterpret_cast<float *>(smem + tc2::kBBytes);
     uint32_t *masks = reinterpret_cast<uint32_t *>(k12 + (size_t)a.g.G * 2 * ROW32);
     uint64_t *d_ready = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
+        smem + ((reinterpret_cast<uint8_t *>(masks + a.g.G) - smem + 7) & ~ptrdiff_t(7)));
     uint64_t *a_ready = d_ready + G * S;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + G * S);
-    Head64P *net64 = reinterpret_cast<Head64P *>(a_ready + G * S + 2);
+    Head64P *net64 = reinterpret_cast<Head64P *>(
+        smem + ((reinterpret_cast<uint8_t *>(a_ready + G * S + 2) - smem + 15) & ~ptrdiff_t(15)));
     float *wo_s = reinterpret_cast<float *>(net64 + 1);          // wo[18], bo
 
     const int tid = threadIdx.x;
@@ -279,13 +292,6 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
         tc2::tmem_st_wait();
         uint64_t *ar = &a_ready[g * S], *dr = &d_ready[g * S];
 
-        // head weights from shared memory (the fp32 copy staged above), so
-        // ptxas keeps them in registers instead of re-loading the constant
-        // bank every config
-        float2 wo2[9];
-#pragma unroll
-        for (int o = 0; o < 9; ++o) wo2[o] = make_float2(wo_s[2 * o], wo_s[2 * o + 1]);
-        const float bo = wo_s[HD];
         int clamps[L];
 #pragma unroll
         for (int l = 0; l < L; ++l) clamps[l] = 0;
@@ -307,6 +313,13 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     p2[w] = make_float2(p[2 * w] + tmp[2 * w], p[2 * w + 1] + tmp[2 * w + 1]);
             }
             const float T_self = (float)a.base_time[self];
+            // head weights from shared memory (the fp32 copy staged above),
+            // re-read per work item (volatile: not hoisted out of the item
+            // loop) so their 19 registers are free in the fp64 tail
+            float2 wo2[9];
+#pragma unroll
+            for (int o = 0; o < 9; ++o) wo2[o] = tc3::lds_f32x2(wo_s + 2 * o);
+            const float bo = tc3::lds_f32x2(wo_s + HD).x;
             const uint32_t krow = tc::smem_u32(k12 + member * ROW32);   // + c * 2 * ROW32 * 4
 
             float best[L], second[L];
@@ -417,9 +430,10 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             for (int l = 0; l < L; ++l) {
                 const bool ambiguous = screen_ambiguous(a, best[l], second[l]);
                 const double tm64 = ambiguous ? 0.0
+                    : C::kNoExact ? (double)best[l]
                     : member_time64_lean(a.t, *net64, a.base_time, self, other, idx[l], member);
                 const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
-                if (live && member == 0) {
+                if (live && member == 0 && !C::kNoWrite) {
                     if (ambiguous) {
                         push_ambiguous(a, l, pl);
                     } else {
@@ -447,6 +461,6 @@ inline size_t tc3_smem_bytes(int n_grid) {
     size_t b = (size_t)tc2::kBBytes;
     b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * 16 * sizeof(uint64_t) + 16 + sizeof(Head64P) + 20 * sizeof(float);
+    b += 2 * 16 * sizeof(uint64_t) + 32 + sizeof(Head64P) + 20 * sizeof(float);
     return b;
 }

@@ -43,11 +43,12 @@ __global__ void __launch_bounds__(tc4::Cfg<G, S>::kThreads, 1)
     float *k12 = reinterpret_cast<float *>(smem + tc2::kBBytes);
     uint32_t *masks = reinterpret_cast<uint32_t *>(k12 + (size_t)a.g.G * 2 * ROW32);
     uint64_t *d_ready = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
+        smem + ((reinterpret_cast<uint8_t *>(masks + a.g.G) - smem + 7) & ~ptrdiff_t(7)));
     uint64_t *a_ready = d_ready + G * S;
     uint64_t *d_free = a_ready + G * S;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d_free + G * S);
-    Head64P *net64 = reinterpret_cast<Head64P *>(d_free + G * S + 2);
+    Head64P *net64 = reinterpret_cast<Head64P *>(
+        smem + ((reinterpret_cast<uint8_t *>(d_free + G * S + 2) - smem + 15) & ~ptrdiff_t(15)));
     float *wo_s = reinterpret_cast<float *>(net64 + 1);
 
     const int tid = threadIdx.x;
@@ -240,6 +241,6 @@ inline size_t tc4_smem_bytes(int n_grid) {
     size_t b = (size_t)tc2::kBBytes;
     b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 3 * 16 * sizeof(uint64_t) + 16 + sizeof(Head64P) + 20 * sizeof(float);
+    b += 3 * 16 * sizeof(uint64_t) + 32 + sizeof(Head64P) + 20 * sizeof(float);
     return b;
 }

@@ -202,9 +202,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     float *k2s = k1s + (size_t)a.g.G * ROW32;
     uint32_t *masks = reinterpret_cast<uint32_t *>(k2s + (size_t)a.g.G * ROW32);
     uint64_t *mbars = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(masks + a.g.G) + 7) & ~uintptr_t(7));
+        smem + ((reinterpret_cast<uint8_t *>(masks + a.g.G) - smem + 7) & ~ptrdiff_t(7)));
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbars + 2 * tc::kGroups);
-    Head64P *net64 = reinterpret_cast<Head64P *>(mbars + 2 * tc::kGroups + 2);
+    Head64P *net64 = reinterpret_cast<Head64P *>(
+        smem + ((reinterpret_cast<uint8_t *>(mbars + 2 * tc::kGroups + 2) - smem + 15) & ~ptrdiff_t(15)));
 
     const int tid = threadIdx.x;
     const int g = tid / tc::kGroupThreads;        // group
@@ -378,6 +379,6 @@ inline size_t tc_smem_bytes(int G) {
     size_t b = (size_t)tc::kGroups * 2 * tc::kTileBytes + tc::kBBytes;
     b += 2 * (size_t)G * ROW32 * sizeof(float) + (size_t)G * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * tc::kGroups * sizeof(uint64_t) + 16 + sizeof(Head64P);
+    b += 2 * tc::kGroups * sizeof(uint64_t) + 32 + sizeof(Head64P);
     return b;
 }

@@ -141,7 +141,7 @@ class SweepPlan:
                  **{f"tcgen05_v4_g{g}s{s}_f{v}": 0x300 | (g << 4) | s | (v << 12)
                     for g, s, v in [(3, 3, v) for v in range(4)] + [(4, 2, v) for v in range(4)]
                     + [(4, 2, 5), (3, 3, 5), (4, 2, 11), (4, 2, 19), (2, 4, 3), (4, 2, 35),
-                       (4, 2, 37), (3, 3, 35)]},
+                       (4, 2, 37), (3, 3, 35), (4, 2, 67), (4, 2, 131), (4, 2, 195)]},
                  # v5 warp-specialized screen (tc4_sweep.cuh)
                  **{f"tcgen05_v5_g{g}s{s}": 0x400 | (g << 4) | s for g, s in ((3, 3), (3, 2), (2, 4), (2, 3))}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
         if kernel not in kinds:
