@@ -1594,6 +1594,57 @@ size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid) {
 }
 
 namespace {
+// Host-call prologue when the caller's inputs sit in pinned (device-mapped)
+// memory: read them over PCIe straight into the workspace and zero the
+// queue / clamp counters -- one launch instead of two H2D copies + a memset.
+__global__ void k_call_begin(const double *__restrict__ hf, const double *__restrict__ hbt,
+                             double *__restrict__ df, double *__restrict__ dbt, int n,
+                             uint32_t *__restrict__ zero, int zero_words) {
+    const int64_t nf = (int64_t)n * NF, total = nf + n + zero_words;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (k < nf) df[k] = hf[k];
+        else if (k < nf + n) dbt[k - nf] = hbt[k - nf];
+        else zero[k - nf - n] = 0u;
+    }
+}
+
+// Host-call epilogue: the small outputs straight into pinned host memory
+// (one launch instead of up to five D2H copies).  Null destinations skipped.
+struct CallEndArgs {
+    const double *solo_time;
+    const int32_t *solo_split, *solo_clamps;
+    const unsigned long long *clamps;
+    const uint32_t *counters;
+    double *h_solo_time;
+    int32_t *h_solo_split, *h_solo_clamps;
+    unsigned long long *h_clamps;
+    uint32_t *h_counters;
+    int64_t LN;
+    int nb;
+};
+__global__ void k_call_end(const CallEndArgs a) {
+    const int64_t total = 3 * a.LN + a.nb + 2;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (k < a.LN) { if (a.h_solo_time) a.h_solo_time[k] = a.solo_time[k]; }
+        else if (k < 2 * a.LN) { if (a.h_solo_split) a.h_solo_split[k - a.LN] = a.solo_split[k - a.LN]; }
+        else if (k < 3 * a.LN) { if (a.h_solo_clamps) a.h_solo_clamps[k - 2 * a.LN] = a.solo_clamps[k - 2 * a.LN]; }
+        else if (k < 3 * a.LN + a.nb) { if (a.h_clamps) a.h_clamps[k - 3 * a.LN] = a.clamps[k - 3 * a.LN]; }
+        else a.h_counters[k - 3 * a.LN - a.nb] = a.counters[k - 3 * a.LN - a.nb];
+    }
+}
+
+// device-visible address of a pinned host buffer, or null (pageable / unknown)
+void *mapped_v(const void *p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+}  // namespace
+
+namespace {
 // The per-call part of cs_build_graph_host (everything after the cached
 // uploads): enqueue only, no synchronization -- so it can be captured.
 int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const double *h_features,
@@ -1776,10 +1827,21 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
 #define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { \
         fprintf(stderr, "cosched_b200: %s\n", cudaGetErrorString(_e)); return CS_ERR_CUDA; } } while (0)
 #define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
-    CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
-    CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    // queue counters and clamp counters are adjacent: one memset
-    CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, (L.clamps - L.qcount) + sizeof(unsigned long long) * nb, st));
+    // queue counters and clamp counters are adjacent: zeroed together
+    const size_t zero_bytes = (L.clamps - L.qcount) + sizeof(unsigned long long) * nb;
+    const double *zf = (const double *)mapped_v(h_features), *zb = (const double *)mapped_v(h_base_time);
+    if (zf && zb) {
+        const int64_t items = (int64_t)n * NF + n + (int64_t)(zero_bytes / 4);
+        int blocks = (int)((items + 255) / 256);
+        if (blocks > sm_count()) blocks = sm_count();
+        k_call_begin<<<blocks, 256, 0, st>>>(zf, zb, (double *)(ws + L.feats), (double *)(ws + L.bt),
+                                             n_apps, (uint32_t *)(ws + L.qcount), (int)(zero_bytes / 4));
+        CS_TRY(cudaGetLastError());
+    } else {
+        CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
+        CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, zero_bytes, st));
+    }
 
     cs_grid dg = *h_grid;
     dg.knob1 = (const double *)(ws + L.knob1);
@@ -1806,12 +1868,30 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));
     if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen, po.corun_chosen, LP, cudaMemcpyDeviceToHost, st));
     if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight, po.weight, 8 * LP, cudaMemcpyDeviceToHost, st));
-    if (h_solo.solo_time) CS_TRY(cudaMemcpyAsync(h_solo.solo_time, so.solo_time, 8 * LN, cudaMemcpyDeviceToHost, st));
-    if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
-    if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
-    if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
-    // queue length + screen-error monitor, checked by the caller after the sync
-    CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
+    // small outputs (+ the queue length / screen-error monitor the caller
+    // checks after the sync): one epilogue kernel when every destination is
+    // pinned, else plain copies
+    CallEndArgs e{so.solo_time, so.solo_split, so.solo_clamps,
+                  (const unsigned long long *)(ws + L.clamps), (const uint32_t *)(ws + L.qcount),
+                  (double *)mapped_v(h_solo.solo_time), (int32_t *)mapped_v(h_solo.solo_split),
+                  (int32_t *)mapped_v(h_solo.solo_clamps), (unsigned long long *)mapped_v(h_clamps),
+                  (uint32_t *)mapped_v(h_counters), (int64_t)LN, nb};
+    const bool zc_out = e.h_counters && (!h_solo.solo_time || e.h_solo_time) &&
+                        (!h_solo.solo_split || e.h_solo_split) &&
+                        (!h_solo.solo_clamps || e.h_solo_clamps) && (!h_clamps || e.h_clamps);
+    if (zc_out) {
+        const int64_t items = 3 * (int64_t)LN + nb + 2;
+        int blocks = (int)((items + 255) / 256);
+        if (blocks > sm_count()) blocks = sm_count();
+        k_call_end<<<blocks, 256, 0, st>>>(e);
+        CS_TRY(cudaGetLastError());
+    } else {
+        if (h_solo.solo_time) CS_TRY(cudaMemcpyAsync(h_solo.solo_time, so.solo_time, 8 * LN, cudaMemcpyDeviceToHost, st));
+        if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
+        if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
+        if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
+        CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
+    }
 #undef CS_TRY
 #undef CS_RC
     return CS_OK;

@@ -80,7 +80,17 @@ class HostGraphCall:
         self._t_ss, self.h_solo_split = _pinned((L, n), torch.int32)
         self.solo = nat.CsSoloOut(nat.ptr(self.h_solo_time), nat.ptr(self.h_solo_split, nat.c_int32_p),
                                   None)
-        self.h_clamps = np.zeros(L, dtype=np.uint64)
+        # pinned like every other buffer: the call's graph reads / writes all
+        # of them with zero-copy kernels or async copies
+        self._t_cl, h_cl = _pinned((L,), torch.int64)
+        self.h_clamps = h_cl.view(np.uint64)
+        self.h_clamps[...] = 0
+        self._stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._net_obj = self.net
+        self._args = (self.net.ref(), ctypes.byref(self.cgrid), nat.ptr(self.h_features),
+                      nat.ptr(self.h_base_time), self.n, self.rel_eps, self.ws_ptr, self.ws_bytes,
+                      nat.ptr(self.h_weights), self.pairs, self.solo,
+                      self.h_clamps.ctypes.data_as(nat.c_ull_p))
 
     def bytes_per_call(self) -> tuple:
         """(H2D bytes, D2H bytes) moved by one repeated call (the grid and the
@@ -98,11 +108,10 @@ class HostGraphCall:
         if base_time is not None:
             self.h_base_time[...] = base_time
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        rc = self.lib.cs_build_graph_host(
-            self.net.ref(), ctypes.byref(self.cgrid), nat.ptr(self.h_features),
-            nat.ptr(self.h_base_time), self.n, self.rel_eps, self.ws_ptr, self.ws_bytes,
-            nat.ptr(self.h_weights), self.pairs, self.solo,
-            self.h_clamps.ctypes.data_as(nat.c_ull_p), stream)
+        if self.net is not self._net_obj or stream != self._stream:
+            self._stream, self._net_obj = stream, self.net
+            self._args = (self.net.ref(),) + self._args[1:]
+        rc = self.lib.cs_build_graph_host(*self._args, stream)
         nat.check(rc, "cs_build_graph_host")
         out = {"weights": self.h_weights, "solo_time": self.h_solo_time,
                "solo_split": self.h_solo_split, "clamps": self.h_clamps}
