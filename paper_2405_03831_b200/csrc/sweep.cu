@@ -667,10 +667,13 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
     __shared__ Head64P net_sm;
     __shared__ double red_v[4];
     __shared__ int red_i[4];
-    // blocks past the (device-side) queue length leave before staging anything
+    // the weights do not depend on the screen: staged before the
+    // programmatic-dependency wait (a no-op without a PDL launch)
+    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // blocks past the (device-side) queue length leave
     const uint32_t count = *a.qcount;
     if (blockIdx.x >= count) return;
-    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t q = blockIdx.x; q < count; q += gridDim.x) {
         const int64_t e = a.queue[q];
@@ -1445,7 +1448,21 @@ int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *
     a.W = d_w;
     // the queue length lives on the device: one resident wave of blocks that
     // stride over it (an oversized grid costs a launch wave per 148 x 16 blocks)
-    k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a, head64_from(n64));
+    // programmatic dependent launch behind the screen (see k_sweep_tc3)
+    const Head64P h64 = head64_from(n64);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sm_count() * 4));
+    cfg.blockDim = dim3(128);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_resolve, a, h64) != cudaSuccess) {
+        cudaGetLastError();
+        k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a, h64);
+    }
     return check_launch();
 }
 }  // namespace

@@ -223,6 +223,10 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
     // programmatic dependent launch: wait for k_tables' results to be visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // a programmatically dependent k_resolve may be scheduled now: its blocks
+    // take SMs this grid leaves free and stage their weights, then wait for
+    // this grid to finish before reading the queue
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int i = tid; i < tc2::kBBytes / 16; i += kThreads)
         reinterpret_cast<uint4 *>(b_tile)[i] =
             reinterpret_cast<const uint4 *>(a.t.w2_tile + tc::kBBytes / 2)[i];
