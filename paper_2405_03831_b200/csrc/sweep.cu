@@ -126,36 +126,6 @@ Head64P head64_from(const Net64P &n) {
     return h;
 }
 
-__device__ __forceinline__ double head64c(const Head64P &net_in, const double (&z)[HD]) {
-    // Launder the weight pointer so the compiler re-reads the (shared-memory)
-    // weights per evaluation instead of hoisting 324 doubles into registers
-    // across calls; k-outer / o-inner keeps 18 independent fp64 chains in
-    // flight (FP64 latency x throughput needs that much ILP), and every chain
-    // still sums over k in the oracle's order (bit-identical results).
-    const Head64P *netp = &net_in;
-    asm volatile("" : "+l"(netp));
-    const Head64P &net = *netp;
-    double acc[HD];
-#pragma unroll
-    for (int o = 0; o < HD; ++o) acc[o] = 0.0;
-#pragma unroll
-    for (int k = 0; k < HD; ++k) {
-        const double hk = z[k] > 0.0 ? z[k] : 0.0;
-#pragma unroll
-        for (int o = 0; o < HD; ++o) acc[o] = fma(hk, net.w2[o * HD + k], acc[o]);
-    }
-    double y = 0.0;
-#pragma unroll
-    for (int o = 0; o < HD; ++o) {
-        const double a2 = acc[o] + net.b2[o];
-        y = fma(a2 > 0.0 ? a2 : 0.0, net.wo[o], y);
-    }
-    y = y + net.bo;
-    return y > 0.0 ? y : 0.0;
-}
-
-// Register-lean variant (three output units per pass) for kernels whose
-// per-thread work is a handful of heads (k_solo): same summation order.
 // Two fp64 weights from shared memory (16 B, broadcast across the warp).
 // Volatile so that the prefetches below stay where they are written:
 // ptxas otherwise sinks each load next to its use at high register pressure
@@ -198,6 +168,34 @@ __device__ __forceinline__ double head64_lean(const Head64P &net, const double (
         acc1 = acc1 + b.y;
         y = fma(acc0 > 0.0 ? acc0 : 0.0, wo.x, y);
         y = fma(acc1 > 0.0 ? acc1 : 0.0, wo.y, y);
+    }
+    y = y + net.bo;
+    return y > 0.0 ? y : 0.0;
+}
+
+// k_resolve's head: k-outer / o-inner, 18 independent fp64 chains (each
+// still sums over k in the oracle's order), weights read as double2 along o
+// from a k-major shared-memory copy `w2t` (w2t[k*18 + o] = w2[o*18 + k]).
+__device__ __forceinline__ double head64t(const Head64P &net, const double *w2t,
+                                          const double (&z)[HD]) {
+    double acc[HD];
+#pragma unroll
+    for (int o = 0; o < HD; ++o) acc[o] = 0.0;
+#pragma unroll
+    for (int k = 0; k < HD; ++k) {
+        const double hk = z[k] > 0.0 ? z[k] : 0.0;
+#pragma unroll
+        for (int o = 0; o < HD; o += 2) {
+            const double2 w = lds_f64x2(w2t + k * HD + o);
+            acc[o] = fma(hk, w.x, acc[o]);
+            acc[o + 1] = fma(hk, w.y, acc[o + 1]);
+        }
+    }
+    double y = 0.0;
+#pragma unroll
+    for (int o = 0; o < HD; ++o) {
+        const double a2 = acc[o] + net.b2[o];
+        y = fma(a2 > 0.0 ? a2 : 0.0, net.wo[o], y);
     }
     y = y + net.bo;
     return y > 0.0 ? y : 0.0;
@@ -253,11 +251,12 @@ __device__ __forceinline__ void z64_row(const cs_tables &t, int self, int other,
 // floor(pred) x T of one member of pair (self, other) under config c
 // (member 0: K1 / view hc, member 1: K2 / reversed partitions)
 __device__ __forceinline__ double member_time64(const cs_tables &t, const Head64P &net,
+                                                const double *w2t,
                                                 const double *__restrict__ base_time, int self,
                                                 int other, int c, int member) {
     double z[HD];
     z64_row(t, self, other, c, member, z);
-    const double y = head64c(net, z);
+    const double y = head64t(net, w2t, z);
     return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
 }
 
@@ -272,10 +271,11 @@ __device__ __forceinline__ double member_time64_lean(const cs_tables &t, const H
 
 // CoRunTime of one config for pair (i, j): max over members (estimator.py:127-129)
 __device__ __forceinline__ double corun64(const cs_tables &t, const Head64P &net,
+                                          const double *w2t,
                                           const double *__restrict__ base_time, int i, int j,
                                           int c) {
-    const double t1 = member_time64(t, net, base_time, i, j, c, 0);
-    const double t2 = member_time64(t, net, base_time, j, i, c, 1);
+    const double t1 = member_time64(t, net, w2t, base_time, i, j, c, 0);
+    const double t2 = member_time64(t, net, w2t, base_time, j, i, c, 1);
     return t1 > t2 ? t1 : t2;
 }
 
@@ -669,7 +669,10 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
     __shared__ int red_i[4];
     // the weights do not depend on the screen: staged before the
     // programmatic-dependency wait (a no-op without a PDL launch)
-    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);
+    __shared__ __align__(16) double w2t[HD * HD];
+    for (int q = threadIdx.x; q < HD * HD; q += blockDim.x)
+        w2t[q] = __ldg(a.t.net_image + kImgHeadOff + (q % HD) * HD + q / HD);
+    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);   // (its __syncthreads covers w2t)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // blocks past the (device-side) queue length leave
     const uint32_t count = *a.qcount;
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
         int arg = INT_MAX;
         for (int c = threadIdx.x; c < a.g.G; c += blockDim.x) {
             if (!((__ldg(a.g.mask + c) >> l) & 1u)) continue;
-            const double tt = corun64(a.t, net64, a.base_time, i, j, c);
+            const double tt = corun64(a.t, net64, w2t, a.base_time, i, j, c);
             if (tt < best) { best = tt; arg = c; }          // ascending c per thread
         }
         for (int off = 16; off; off >>= 1) {
