@@ -104,17 +104,62 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    NVML in a background thread every 5 ms, plus one sample as the region
+    opens and one as it closes, so even a 0.1 s region is covered (an
+    nvidia-smi subprocess needs ~100 ms to print its first line).  Falls back
+    to `nvidia-smi -lms 100` when NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.nvml = None
+        self.samples = []             # (sm_mhz, max_mhz, reasons bitmask)
+        self.lines = []
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.nvml = pynvml
+            self.bits = {
+                "hw_slowdown": getattr(pynvml, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi below
+            self.nvml = None
+
+    def _sample(self):
+        nv = self.nvml
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+            smax = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+            try:
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+            except Exception:  # noqa: BLE001 -- older bindings
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+            self.samples.append((float(sm), float(smax), int(rs)))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _loop(self):
+        while not self._stop.wait(0.005):
+            self._sample()
 
     def __enter__(self):
+        if self.nvml is not None:
+            import threading
+            self._stop = threading.Event()
+            self._sample()
+            self._thread = threading.Thread(target=self._loop, daemon=True)
+            self._thread.start()
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
@@ -125,7 +170,11 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        if self.nvml is not None:
+            self._sample()
+            self._stop.set()
+            self._thread.join(timeout=1)
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -137,8 +186,13 @@ class ClockSampler:
 
     def summary(self) -> dict:
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
+        for f, fmax, rs in self.samples:
+            sm.append(f)
+            smax = fmax
+            for name in self.NAMES:
+                if rs & self.bits[name]:
+                    reasons.add(name)
+        for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -147,11 +201,12 @@ class ClockSampler:
                 smax = float(parts[2])
             except ValueError:
                 continue
-            for name, val in zip(names, parts[5:9]):
+            for name, val in zip(self.NAMES, parts[5:9]):
                 if val.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml (5 ms)" if self.nvml is not None else "nvidia-smi (100 ms)"}
 
 
 # --------------------------------------------------------------------------
