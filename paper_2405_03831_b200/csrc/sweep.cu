@@ -441,6 +441,8 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
         for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / 8); i += blockDim.x)
             hd[i] = __ldg(img + kImgHeadOff + i);
     }
+    // the image predates the previous kernel; the features may come from it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     const Net64P &net = sm.net;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1155,8 +1157,23 @@ int launch_tables(const cs_network *net, const double *d_features, int32_t n_app
     int64_t threads = items > W2_TILE_ELEMS ? items : W2_TILE_ELEMS;
     int blocks = (int)((threads + 127) / 128);
     if (blocks > sm_count() * 16) blocks = sm_count() * 16;
-    k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables,
-                                                        d_base_time, solo, do_solo);
+    // programmatic dependent launch: the blocks stage the network image
+    // while the previous kernel (the host call's input prologue) finishes
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(128);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_tables, np, d_features, n_apps, g, *tables, d_base_time, solo,
+                           do_solo) != cudaSuccess) {
+        cudaGetLastError();
+        k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables,
+                                                            d_base_time, solo, do_solo);
+    }
     return check_launch();
 }
 }  // namespace
@@ -1620,6 +1637,7 @@ namespace {
 __global__ void k_call_begin(const double *__restrict__ hf, const double *__restrict__ hbt,
                              double *__restrict__ df, double *__restrict__ dbt, int n,
                              uint32_t *__restrict__ zero, int zero_words) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // k_tables may stage now
     const int64_t nf = (int64_t)n * NF, total = nf + n + zero_words;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
