@@ -1726,7 +1726,10 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     // The knob grid, the network image and the zeroed matrix persist in the
     // workspace between calls: re-upload only what changed since the last
     // call on this workspace (host-side record per workspace pointer).
-    std::vector<uint8_t> key;
+    // (per-thread buffer: no allocation per call once it has grown)
+    thread_local std::vector<uint8_t> key_buf;
+    std::vector<uint8_t> &key = key_buf;
+    key.clear();
     {
         auto put = [&key](const void *p, size_t bytes) {
             const uint8_t *b = (const uint8_t *)p;
