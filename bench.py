@@ -472,10 +472,7 @@ def run_ours(args):
                          "unit": "TFLOP/s", "frac": achieved_tflops / tf,
                          "traffic": measured_traffic(args.workload, args.kernel),
                          "kernel": {"tcgen05": "k_sweep_tc3<L,4,2,3> (tcgen05, A in TMEM, v4)",
-                                    "tcgen05_v3": "k_sweep_tc2<L,4,2> (tcgen05, A in TMEM, v3)",
-                                    "simt": "k_sweep (SIMT fp32)",
-                                    "tcgen05_smem": "k_sweep_tc (tcgen05, A in SMEM)"}.get(
-                                        args.kernel, args.kernel), "kernel_ms": sweep_avg,
+                                    "simt": "k_sweep (SIMT fp32)"}[args.kernel], "kernel_ms": sweep_avg,
                          "flops_per_unit": FLOPS_PER_UNIT, "units_per_launch": units_local,
                          "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
                          "kernel_share_of_step": sweep_avg / (total_ms / args.steps)},
@@ -576,14 +573,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--workload", default="n256", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "tcgen05_v3", "tcgen05_smem", "simt", "tcgen05_g4s2",
-                             "tcgen05_g3s3", "tcgen05_g2s4", "tcgen05_v4_g3s3",
-                             "tcgen05_v4_g4s2"] + [f"tcgen05_v4_g{g}s{s}_f{v}" for g, s in
-                                                   ((3, 3), (4, 2)) for v in range(4)]
-                    + ["tcgen05_v4_g4s2_f5", "tcgen05_v4_g3s3_f5", "tcgen05_v4_g4s2_f11",
-                       "tcgen05_v4_g4s2_f19", "tcgen05_v4_g2s4_f3", "tcgen05_v4_g4s2_f35",
-                       "tcgen05_v4_g4s2_f37", "tcgen05_v4_g3s3_f35", "tcgen05_v5_g3s3",
-                       "tcgen05_v5_g3s2", "tcgen05_v5_g2s4", "tcgen05_v5_g2s3"],
+    ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "simt"],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

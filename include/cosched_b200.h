@@ -67,8 +67,8 @@ enum {
     CS_KERNEL_AUTO = 0,          /* tcgen05 on sm_100a                                    */
     CS_KERNEL_TCGEN05 = 1,       /* layer 2 on tensor cores, A operand in TMEM, fp16 3-term
                                     split, fp32 accumulate                                */
-    CS_KERNEL_SIMT = 2,          /* layer 2 as fp32 FFMA with W2 in the parameter bank    */
-    CS_KERNEL_TCGEN05_SMEM_A = 3 /* tensor cores with the A operand staged in SMEM (v2)   */
+    CS_KERNEL_SIMT = 2           /* layer 2 as fp32 FFMA with W2 in the parameter bank
+                                    (also the fallback for networks beyond fp16 range)   */
 };
 
 /* NetworkWeights (fnn.py:42-68), HOST fp64, row-major exactly as the
@@ -197,8 +197,8 @@ int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32
                    int32_t n_apps, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
                    unsigned long long *d_clamps, double *d_w, void *stream);
 
-/* The pair sweep in TWO launches (tcgen05 v4 screen only: CS_KERNEL_AUTO /
- * CS_KERNEL_TCGEN05 or a 0xV3GS variant): the screen decides every
+/* The pair sweep in TWO launches (tcgen05 screen only: CS_KERNEL_AUTO /
+ * CS_KERNEL_TCGEN05): the screen decides every
  * unambiguous (pair, budget) itself -- co-run vs time-share against
  * d_solo_time (cs_prepare / cs_solo, stream-ordered before) and the scatter
  * into d_w (L x N x N, zeroed once by the caller; NULL to skip) -- and k_resolve

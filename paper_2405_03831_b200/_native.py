@@ -20,7 +20,7 @@ SWEEP_LIB = os.path.join(_HERE, "libcosched_b200.so")
 MATCH_LIB = os.path.join(_HERE, "libcosched_match.so")
 
 MAX_BUDGETS = 8
-KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT, KERNEL_TCGEN05_SMEM_A = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT = 0, 1, 2
 _lock = threading.Lock()
 _libs: dict = {}
 

@@ -38,7 +38,7 @@ constexpr int NF = CS_NUM_FEATURES;
 constexpr int HD = CS_HIDDEN;
 constexpr int IN = CS_INPUT_DIM;
 constexpr int ROW32 = 20;                  // fp32 table row: 18 + 2 pad (80 B, float4-aligned)
-constexpr int W2_TILE_ELEMS = 2 * 32 * 64; // fp16 B operands: v2 tile | v3 slices
+constexpr int W2_TILE_ELEMS = 4 * 32 * 16; // fp16 B operands: 4 K-slices of W2 (tcgen05_util.cuh)
 constexpr double FLOOR = 0.5;              // estimator.py:33
 constexpr int kSweepThreads = 128;
 
@@ -372,10 +372,8 @@ __device__ __forceinline__ void load_row20(const float *__restrict__ p, float (&
     r[16] = v4.x; r[17] = v4.y;
 }
 
-#include "tc_sweep.cuh"
-#include "tc2_sweep.cuh"
+#include "tcgen05_util.cuh"
 #include "tc3_sweep.cuh"
-#include "tc4_sweep.cuh"
 
 // ---- k_tables: factored layer 1 (core.py:367-377 + fnn.py:163) ------------
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
@@ -446,8 +444,7 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
     __syncthreads();
     const Net64P &net = sm.net;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid < W2_TILE_ELEMS / 2) write_b_tile(net, t.w2_tile, (int)tid);
-    else if (tid < W2_TILE_ELEMS) write_b_slices(net, t.w2_tile + W2_TILE_ELEMS / 2, (int)tid - W2_TILE_ELEMS / 2);
+    if (tid < W2_TILE_ELEMS) write_b_slices(net, t.w2_tile, (int)tid);
     const int lane = threadIdx.x & 31;
     const int h = lane < HD ? lane : HD - 1;
     const int64_t rows = (int64_t)n + g.G + g.S;
@@ -972,100 +969,48 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
         return CS_OK;
     }
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
-    int64_t ctas = (nblocks + tc::kGroups - 1) / tc::kGroups;
-    if (ctas > sm_count()) ctas = sm_count();
-    if (kind == CS_KERNEL_TCGEN05_SMEM_A) {
-        const size_t smem = tc_smem_bytes(a.g.G);
-        if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
-        if (cudaFuncSetAttribute(k_sweep_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-            return CS_ERR_CUDA;
-        k_sweep_tc<L><<<(unsigned)ctas, tc::kThreads, smem, st>>>(a, net, h64);
-        return CS_OK;
-    }
-    if ((kind & 0xF00) == 0x400) {
-        // v5 warp-specialized screen (tc4_sweep.cuh): 0x4GS
-        const int G = (kind >> 4) & 0xF, S = kind & 0xF;
-        const size_t smem = tc4_smem_bytes(a.g.G);
-        if (smem > 227 * 1024) return CS_ERR_ARG;
-        auto go4 = [&](auto kern, int groups, int threads) -> int {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                cudaSuccess)
-                return CS_ERR_CUDA;
-            int64_t c = (nblocks + groups - 1) / groups;
-            if (c > sm_count()) c = sm_count();
-            kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
-            return CS_OK;
-        };
-#define CS_TC4(GG, SS) \
-        if (G == GG && S == SS) return go4(k_sweep_tc4<L, GG, SS>, GG, tc4::Cfg<GG, SS>::kThreads);
-        CS_TC4(3, 3) CS_TC4(3, 2) CS_TC4(2, 4) CS_TC4(2, 3)
-#undef CS_TC4
-        return CS_ERR_ARG;
-    }
-    if (kind == CS_KERNEL_TCGEN05 || (kind & 0xF00) == 0x300) {
-        // v4 screen (tc3_sweep.cuh); 0xV3GS kinds select a (groups, stages,
-        // variant flags) instance for tuning
-        // default: 4 groups x 2 stages, per-group issuer warps, elected arrives
-        if (kind == CS_KERNEL_TCGEN05) kind = 0x3342;
-        const int G = (kind >> 4) & 0xF, S = kind & 0xF;
-        const size_t smem = tc3_smem_bytes(a.g.G);
-        if (smem > 227 * 1024) return CS_ERR_ARG;
-        auto go3 = [&](auto kern, int groups, int threads) -> int {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                cudaSuccess)
-                return CS_ERR_CUDA;
-            int64_t c = (nblocks + groups - 1) / groups;
-            if (c > sm_count()) c = sm_count();
-            // programmatic dependent launch: the CTAs' prologue (TMEM allocation,
-            // mbarrier init) overlaps the tail of k_tables; the kernel waits on
-            // griddepcontrol.wait before it reads anything k_tables wrote
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)c);
-            cfg.blockDim = dim3((unsigned)threads);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = st;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            if (cudaLaunchKernelEx(&cfg, kern, a, net, h64) != cudaSuccess) {
-                cudaGetLastError();
-                kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
-            }
-            return CS_OK;
-        };
-        const int V = (kind >> 12) & 0xFF;
-#define CS_TC3(GG, SS, VV) \
-        if (G == GG && S == SS && V == VV) \
-            return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
-        CS_TC3(3, 3, 0) CS_TC3(3, 3, 1) CS_TC3(3, 3, 2) CS_TC3(3, 3, 3)
-        CS_TC3(4, 2, 0) CS_TC3(4, 2, 1) CS_TC3(4, 2, 2) CS_TC3(4, 2, 3)
-        CS_TC3(4, 2, 5) CS_TC3(3, 3, 5) CS_TC3(4, 2, 11) CS_TC3(4, 2, 19) CS_TC3(2, 4, 3)
-        CS_TC3(4, 2, 35) CS_TC3(4, 2, 37) CS_TC3(3, 3, 35)
-        CS_TC3(4, 2, 67) CS_TC3(4, 2, 131) CS_TC3(4, 2, 195)
-#undef CS_TC3
-        return CS_ERR_ARG;
-    }
-    const size_t smem = tc2_smem_bytes(a.g.G);
-    if (smem > 227 * 1024) return CS_ERR_ARG;
-    // (compute groups, pipeline stages) variants of the v3 TMEM-A screen
-    // (tc2_sweep.cuh), selected by 0x1GS kinds for comparison
-    int G = 4, S = 2;
-    if ((kind & 0xF00) == 0x100) { G = (kind >> 4) & 0xF; S = kind & 0xF; }
-    auto go = [&](auto kern, int groups, int threads) -> int {
+    if (kind != CS_KERNEL_TCGEN05 && (kind & 0xF00) != 0x300) return CS_ERR_ARG;
+    // default: 4 compute groups x 2 TMEM stages, per-group issuer warps,
+    // elected a_ready arrives (0x3342); 0xV3GS kinds select the timing-probe
+    // instances compiled with -DCS_TIMING_PROBES (tools/, never the product)
+    if (kind == CS_KERNEL_TCGEN05) kind = 0x3342;
+    const int G = (kind >> 4) & 0xF, S = kind & 0xF;
+    const size_t smem = tc3_smem_bytes(a.g.G);
+    if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
+    auto go3 = [&](auto kern, int groups, int threads) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return CS_ERR_CUDA;
         int64_t c = (nblocks + groups - 1) / groups;
         if (c > sm_count()) c = sm_count();
-        kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
+        // programmatic dependent launch: the CTAs' prologue (TMEM allocation,
+        // mbarrier init) overlaps the tail of k_tables; the kernel waits on
+        // griddepcontrol.wait before it reads anything k_tables wrote
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, a, net, h64) != cudaSuccess) {
+            cudaGetLastError();
+            kern<<<(unsigned)c, threads, smem, st>>>(a, net, h64);
+        }
         return CS_OK;
     };
-    if (G == 4 && S == 2) return go(k_sweep_tc2<L, 4, 2>, 4, Tc2Cfg<4, 2>::kThreads);
-    if (G == 3 && S == 3) return go(k_sweep_tc2<L, 3, 3>, 3, Tc2Cfg<3, 3>::kThreads);
-    if (G == 2 && S == 4) return go(k_sweep_tc2<L, 2, 4>, 2, Tc2Cfg<2, 4>::kThreads);
+    const int V = (kind >> 12) & 0xFF;
+#define CS_TC3(GG, SS, VV) \
+    if (G == GG && S == SS && V == VV) \
+        return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
+    CS_TC3(4, 2, 3)
+#ifdef CS_TIMING_PROBES
+    CS_TC3(4, 2, 19) CS_TC3(4, 2, 67) CS_TC3(4, 2, 131) CS_TC3(4, 2, 195)
+#endif
+#undef CS_TC3
     return CS_ERR_ARG;
 }
 
@@ -1244,9 +1189,7 @@ int cs_pair_screen_fused(const cs_network *net, const cs_tables *tables, const c
                          int kernel_kind, void *stream) {
     if (!d_solo_time || !out.corun_chosen || !out.weight || !d_queue) return CS_ERR_ARG;
     if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
-    if (kernel_kind != CS_KERNEL_TCGEN05 && (kernel_kind & 0xF00) != 0x300 &&
-        (kernel_kind & 0xF00) != 0x400)
-        return CS_ERR_ARG;
+    if (kernel_kind != CS_KERNEL_TCGEN05 && (kernel_kind & 0xF00) != 0x300) return CS_ERR_ARG;
     return pair_screen_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
                             d_queue, d_queue_count, d_clamps, kernel_kind, d_solo_time,
                             d_solo_clamps, d_w, 1, stream);
@@ -1366,8 +1309,7 @@ int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_gr
         kernel_kind = (zmax < 30000.0 && wmax < 30000.0) ? CS_KERNEL_TCGEN05 : CS_KERNEL_SIMT;
     }
     if (kernel_kind != CS_KERNEL_TCGEN05 && kernel_kind != CS_KERNEL_SIMT &&
-        kernel_kind != CS_KERNEL_TCGEN05_SMEM_A && (kernel_kind & 0xF00) != 0x100 &&
-        (kernel_kind & 0xF00) != 0x300 && (kernel_kind & 0xF00) != 0x400)
+        (kernel_kind & 0xF00) != 0x300)
         return CS_ERR_ARG;
     int lrc;
     switch (a.g.L) {

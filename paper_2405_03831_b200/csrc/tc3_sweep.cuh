@@ -33,14 +33,22 @@ struct Cfg {
     static constexpr bool kPerGroupIssuer = (V & 2) != 0;
     static constexpr bool kComputeIssue = (V & 4) != 0;
     static constexpr bool kIssuerSpin = (V & 8) != 0;   // issuer polls instead of sleeping
+#ifdef CS_TIMING_PROBES
     static constexpr bool kNoTensor = (V & 16) != 0;    // TIMING PROBE ONLY: no MMAs, no waits
+#else
+    static constexpr bool kNoTensor = false;            // probes exist only in tool builds
+#endif
     // bit 5: read D(c) into registers, then build A(c+S) into the freed stage
     // BEFORE the epilogue math of c -- MMA(c+S) is issued one epilogue earlier
     static constexpr bool kEarlyIssue = (V & 32) != 0;
     // TIMING PROBES ONLY (wrong results): bit 6 skips the fp64 winner
     // re-evaluation, bit 7 skips the record / matrix writes of the tail
+#ifdef CS_TIMING_PROBES
     static constexpr bool kNoExact = (V & 64) != 0;
     static constexpr bool kNoWrite = (V & 128) != 0;
+#else
+    static constexpr bool kNoExact = false, kNoWrite = false;
+#endif
     static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
     static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
@@ -127,7 +135,7 @@ __device__ __forceinline__ void issue_config(uint32_t d_t, uint32_t a_t, uint64_
 }
 
 // this thread's A row of one config (20 live 32-bit TMEM columns, layout of
-// tc2_sweep.cuh), stored into its TMEM lane
+// tcgen05_util.cuh), stored into its TMEM lane
 __device__ __forceinline__ float4 lds4(uint32_t a) {
     float4 v;
     asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int i = tid; i < tc2::kBBytes / 16; i += kThreads)
         reinterpret_cast<uint4 *>(b_tile)[i] =
-            reinterpret_cast<const uint4 *>(a.t.w2_tile + tc::kBBytes / 2)[i];
+            reinterpret_cast<const uint4 *>(a.t.w2_tile)[i];
     for (int i = tid; i < a.g.G * ROW32; i += kThreads) {
         const int c = i / ROW32, h = i - c * ROW32;
         k12[(2 * c) * ROW32 + h] = a.t.knob1_32[i];

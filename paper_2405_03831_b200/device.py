@@ -131,19 +131,9 @@ class SweepPlan:
         if not 0 <= pair_begin <= pair_end <= P_all:
             raise ValidationError(f"pair range [{pair_begin}, {pair_end}) outside [0, {P_all})")
         self.n, self.grid, self.rel_eps = n, grid, float(rel_eps)
-        kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT,
-                 "tcgen05_smem": nat.KERNEL_TCGEN05_SMEM_A,
-                 # (compute groups, pipeline stages) variants of the v3 TMEM-A screen
-                 "tcgen05_v3": 0x142, "tcgen05_g4s2": 0x142,
-                 # (groups, stages) variants of the v4 screen (tc3_sweep.cuh)
-                 "tcgen05_v4_g3s3": 0x333, "tcgen05_v4_g4s2": 0x342,
-                 # + flags: 0x1000 elected a_ready arrive, 0x2000 per-group issuer warps
-                 **{f"tcgen05_v4_g{g}s{s}_f{v}": 0x300 | (g << 4) | s | (v << 12)
-                    for g, s, v in [(3, 3, v) for v in range(4)] + [(4, 2, v) for v in range(4)]
-                    + [(4, 2, 5), (3, 3, 5), (4, 2, 11), (4, 2, 19), (2, 4, 3), (4, 2, 35),
-                       (4, 2, 37), (3, 3, 35), (4, 2, 67), (4, 2, 131), (4, 2, 195)]},
-                 # v5 warp-specialized screen (tc4_sweep.cuh)
-                 **{f"tcgen05_v5_g{g}s{s}": 0x400 | (g << 4) | s for g, s in ((3, 3), (3, 2), (2, 4), (2, 3))}, "tcgen05_g3s3": 0x133, "tcgen05_g2s4": 0x124}
+        # the tcgen05 screen (k_sweep_tc3) or the fp32 SIMT screen (k_sweep); both feed
+        # the same exact fp64 steps, so results are identical
+        kinds = {"tcgen05": nat.KERNEL_TCGEN05, "simt": nat.KERNEL_SIMT}
         if kernel not in kinds:
             raise ValueError(f"kernel must be one of {sorted(kinds)}, got {kernel!r}")
         if kernel == "tcgen05" and not fp16_screen_safe(weights):
@@ -208,10 +198,10 @@ class SweepPlan:
             ctypes.cast(_dptr(self.solo_split), nat.c_int32_p),
             ctypes.cast(_dptr(self.solo_clamps), nat.c_int32_p))
         self._side = torch.cuda.Stream(self.device)
-        # the v4 tcgen05 screen runs the fused pipeline: k_tables (+ solo
+        # the tcgen05 screen runs the fused pipeline: k_tables (+ solo
         # splits) -> k_sweep_tc3 (+ decide/scatter) -> k_resolve (+ decide);
         # the other screens keep tables | solo -> screen -> resolve -> decide
-        self.fused = kernel == "tcgen05" or kernel.startswith(("tcgen05_v4", "tcgen05_v5"))
+        self.fused = kernel == "tcgen05"
         self.launches_per_run = 3 if self.fused else 5
 
     # ------------------------------------------------------------------
