@@ -26,10 +26,12 @@
  *                     solo, sweep, resolve, scatter, D2H) in one call.
  *
  * Conventions: every `d_` pointer is device memory owned by the caller; every
- * `h_` pointer is host memory (pinned for overlap, pageable works).  Nothing
- * allocates; calls are stream-ordered on `stream` (a cudaStream_t, NULL =
- * legacy default stream) and only cs_build_graph_host synchronizes.  No global
- * mutable state: calls are re-entrant across host threads and devices.
+ * `h_` pointer is host memory (pinned for overlap, pageable works).  Only
+ * cs_device_alloc and cs_workspace_retain allocate; calls are stream-ordered on `stream` (a cudaStream_t, NULL =
+ * legacy default stream) and only cs_build_graph_host synchronizes.  The only
+ * state kept between calls is that of workspaces the caller explicitly
+ * retains (cs_workspace_retain); calls are re-entrant across host threads
+ * and devices.
  * Return value: 0 on success, a negative CS_ERR_* code otherwise.
  *
  * Pairs are unordered (i < j) in row-major order, linear index
@@ -276,13 +278,21 @@ int cs_device_alloc(size_t bytes, void **d_out);
 int cs_device_free(void *d_ptr);
 
 size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid);
+/* Optional persistence of a cs_build_graph_host workspace.  After
+ * cs_workspace_retain the library keeps the knob grid, the network image and
+ * the zeroed matrix resident in d_workspace, re-uploads only what changed, and
+ * replays repeated identical calls (pinned host buffers, non-default stream)
+ * as a CUDA graph (at most 4 per workspace, LRU).  The caller must not write
+ * the workspace between calls and must call cs_workspace_release before
+ * freeing it (cs_device_free does so).  A workspace that was never retained
+ * is uploaded into on every call and carries no state between calls.  One
+ * call at a time per workspace (calls on one retained workspace serialize). */
+int cs_workspace_retain(void *d_workspace, size_t workspace_bytes);
+int cs_workspace_release(void *d_workspace);
 /* h_weights: L x N x N (NULL to skip); h_pairs members: L x P host arrays
  * (NULL members skipped); h_solo members: L x N host arrays (NULL skipped);
- * h_clamps: L (NULL to skip).  Full graph (all P pairs).  The knob grid, the
- * network image and the zeroed matrix persist in d_workspace: a call that
- * repeats the previous call's grid/network on the same workspace uploads only
- * the per-call inputs (a host-side record per workspace pointer; the
- * workspace must not be written by anything else between calls). */
+ * h_clamps: L (NULL to skip).  Full graph (all P pairs).  Synchronizes
+ * `stream` before returning. */
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                         const double *h_base_time, int32_t n_apps, double rel_eps,
                         void *d_workspace, size_t workspace_bytes, double *h_weights,

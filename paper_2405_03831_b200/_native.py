@@ -144,6 +144,8 @@ SWEEP_SYMBOLS = {
                                        ctypes.c_void_p, ctypes.c_void_p]),
     "cs_device_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "cs_device_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "cs_workspace_retain": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
+    "cs_workspace_release": (ctypes.c_int, [ctypes.c_void_p]),
     "cs_build_graph_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.POINTER(CsGrid)]),
     "cs_build_graph_host": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsGrid),
                                            c_double_p, c_double_p, ctypes.c_int32,

@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -1563,6 +1564,9 @@ int cs_device_alloc(size_t bytes, void **d_out) {
 }
 
 int cs_device_free(void *d_ptr) {
+    // a workspace retained for cs_build_graph_host loses its state first, so a
+    // later allocation at the same address can never inherit it
+    cs_workspace_release(d_ptr);
     if (d_ptr && cudaFree(d_ptr) != cudaSuccess) return CS_ERR_CUDA;
     return CS_OK;
 }
@@ -1634,7 +1638,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
                        cudaStream_t st);
 
 struct HostCallKey {
-    const void *ws, *f, *bt, *w, *p0, *p1, *p2, *p3, *s0, *s1, *s2, *cl, *stream;
+    const void *f, *bt, *w, *p0, *p1, *p2, *p3, *s0, *s1, *s2, *cl, *stream;
     int32_t n;
     double eps;
     bool operator==(const HostCallKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
@@ -1642,9 +1646,76 @@ struct HostCallKey {
 struct HostCallGraph {
     HostCallKey key;
     cudaGraphExec_t exec = nullptr;
-    int hits = 0;
+    int hits = 0;            // identical calls seen; capture on the second
+    bool failed = false;     // capture failed once: this key stays on the direct path
+    uint64_t used = 0;       // LRU stamp
 };
+constexpr size_t kMaxGraphsPerWorkspace = 4;
+
+// State of a workspace the caller declared persistent (cs_workspace_retain):
+// what was last uploaded into it, one pinned counter slot, and the CUDA
+// graphs of its repeated calls.  Freed by cs_workspace_release (which
+// cs_device_free calls), so no state outlives the allocation.
+struct WorkspaceState {
+    size_t bytes = 0;
+    std::vector<uint8_t> key;      // grid + network + sizes of the resident uploads; empty = none
+    uint32_t *h_counters = nullptr;
+    std::vector<HostCallGraph> graphs;
+    uint64_t clock = 0;
+    std::mutex mu;                 // one call at a time per workspace
+};
+std::mutex g_ws_mu;
+std::unordered_map<const void *, std::shared_ptr<WorkspaceState>> g_ws;
+
+void drop_graphs(WorkspaceState &w) {
+    for (auto &g : w.graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    w.graphs.clear();
+}
 }  // namespace
+
+int cs_workspace_retain(void *d_workspace, size_t workspace_bytes) {
+    if (!d_workspace || ((uintptr_t)d_workspace & 255) || !workspace_bytes) return CS_ERR_ARG;
+    auto st = std::make_shared<WorkspaceState>();
+    st->bytes = workspace_bytes;
+    if (cudaHostAlloc((void **)&st->h_counters, sizeof(uint32_t) * 2, cudaHostAllocDefault) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return CS_ERR_CUDA;
+    }
+    std::shared_ptr<WorkspaceState> old;
+    {
+        std::lock_guard<std::mutex> lock(g_ws_mu);
+        auto &slot = g_ws[d_workspace];
+        old.swap(slot);
+        slot = st;
+    }
+    if (old) {
+        std::lock_guard<std::mutex> lock(old->mu);
+        drop_graphs(*old);
+        cudaFreeHost(old->h_counters);
+        old->h_counters = nullptr;
+    }
+    return CS_OK;
+}
+
+int cs_workspace_release(void *d_workspace) {
+    if (!d_workspace) return CS_OK;
+    std::shared_ptr<WorkspaceState> st;
+    {
+        std::lock_guard<std::mutex> lock(g_ws_mu);
+        auto it = g_ws.find(d_workspace);
+        if (it == g_ws.end()) return CS_OK;
+        st = it->second;
+        g_ws.erase(it);
+    }
+    std::lock_guard<std::mutex> lock(st->mu);   // waits out a call in flight on it
+    drop_graphs(*st);
+    if (st->h_counters) cudaFreeHost(st->h_counters);
+    st->h_counters = nullptr;
+    st->key.clear();
+    return CS_OK;
+}
 
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                         const double *h_base_time, int32_t n_apps, double rel_eps,
@@ -1657,19 +1728,28 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     const GraphLayout L = graph_layout(n_apps, h_grid);
     if (workspace_bytes < L.total) return CS_ERR_WORKSPACE;
     if ((uintptr_t)d_workspace & 255) return CS_ERR_ARG;
+    Net64P np;
+    if (!net64_from(net, &np)) return CS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     char *ws = (char *)d_workspace;
-    const int64_t P = (int64_t)n_apps * (n_apps - 1) / 2;
     const int nb = h_grid->n_budgets, G = h_grid->n_grid, S = h_grid->solo_offsets[nb];
     const size_t n = (size_t)n_apps;
-#define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { \
+#define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { cudaGetLastError(); \
         fprintf(stderr, "cosched_b200: %s\n", cudaGetErrorString(_e)); return CS_ERR_CUDA; } } while (0)
 #define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
-    // The knob grid, the network image and the zeroed matrix persist in the
-    // workspace between calls: re-upload only what changed since the last
-    // call on this workspace (host-side record per workspace pointer).
-    // (per-thread buffer: no allocation per call once it has grown)
-    thread_local std::vector<uint8_t> key_buf;
+    // A retained workspace (cs_workspace_retain) keeps the knob grid, the
+    // network image and the zeroed matrix between calls and re-uploads only
+    // what changed; any other workspace is uploaded into on every call.
+    std::shared_ptr<WorkspaceState> state;
+    {
+        std::lock_guard<std::mutex> lock(g_ws_mu);
+        auto it = g_ws.find(d_workspace);
+        if (it != g_ws.end() && it->second->bytes == workspace_bytes) state = it->second;
+    }
+    std::unique_lock<std::mutex> call_lock;
+    if (state) call_lock = std::unique_lock<std::mutex>(state->mu);
+    if (state && !state->h_counters) state.reset();   // released while we waited
+    thread_local std::vector<uint8_t> key_buf;      // no allocation per call once grown
     std::vector<uint8_t> &key = key_buf;
     key.clear();
     {
@@ -1685,28 +1765,14 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
             put(h_grid->mask, sizeof(uint32_t) * G);
         }
         if (S) put(h_grid->solo_knob, sizeof(double) * S * 4);
-        Net64P np;
-        if (!net64_from(net, &np)) return CS_ERR_ARG;
         put(&np, sizeof(np));
-        put(&workspace_bytes, sizeof(workspace_bytes));
     }
-    static std::mutex cache_mu;
-    static std::unordered_map<const void *, std::vector<uint8_t>> cache;
-    // one pinned 2-word counter slot per workspace (read back inside the call
-    // and its graph; lives as long as the process)
-    static std::unordered_map<const void *, uint32_t *> counters;
-    bool fresh;
-    uint32_t *h_counters = nullptr;
-    {
-        std::lock_guard<std::mutex> lock(cache_mu);
-        auto it = cache.find(d_workspace);
-        fresh = it == cache.end() || it->second != key;
-        if (fresh) cache[d_workspace] = key;   // recorded before the upload: a failure below
-        uint32_t *&slot = counters[d_workspace];   // returns an error and the caller retries
-        if (!slot) CS_TRY(cudaHostAlloc((void **)&slot, sizeof(uint32_t) * 2, cudaHostAllocDefault));
-        h_counters = slot;
-    }
+    const bool fresh = !state || state->key != key;
     if (fresh) {
+        if (state) {
+            state->key.clear();       // recorded again only once the uploads went through
+            drop_graphs(*state);      // captured graphs carry the old grid / network
+        }
         if (G) {
             CS_TRY(cudaMemcpyAsync(ws + L.knob1, h_grid->knob1, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
             CS_TRY(cudaMemcpyAsync(ws + L.knob2, h_grid->knob2, sizeof(double) * G * 4, cudaMemcpyHostToDevice, st));
@@ -1715,45 +1781,48 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
         if (S) CS_TRY(cudaMemcpyAsync(ws + L.solo_knob, h_grid->solo_knob, sizeof(double) * S * 4, cudaMemcpyHostToDevice, st));
         // the sweep writes every off-diagonal entry each call; the diagonal stays 0
         CS_TRY(cudaMemsetAsync(ws + L.W, 0, sizeof(double) * n * n * nb, st));
-    }
-    if (fresh) {
         // network image into the workspace's tables (pageable copy, outside any graph)
         cs_tables t;
         CS_RC(cs_tables_bind(ws + L.tables, cs_tables_bytes(n_apps, G, S), n_apps, G, S, &t));
         CS_RC(cs_tables_set_network(net, &t, stream));
     }
-    // Per-call work: replayed as a CUDA graph once the same call (workspace,
-    // host buffers, stream) repeats -- one launch instead of ~15 API calls.
-    // Host buffers must be pinned for the graph (a capture with pageable
-    // memory fails and the call stays on the direct path).
-    HostCallKey key2{d_workspace, h_features, h_base_time, h_weights,
+    uint32_t *h_counters = state ? state->h_counters : nullptr;
+    // Per-call work: replayed as a CUDA graph once the same call (retained
+    // workspace, pinned host buffers, same non-default stream) repeats -- one
+    // launch instead of ~15 API calls.  Pageable inputs or the legacy stream
+    // never try a capture.
+    HostCallKey key2{h_features, h_base_time, h_weights,
                      h_pairs.corun_grid_index, h_pairs.corun_time, h_pairs.corun_chosen,
                      h_pairs.weight, h_solo.solo_time, h_solo.solo_split, h_solo.solo_clamps,
                      h_clamps, stream, n_apps, rel_eps};
-    static std::mutex graph_mu;
-    static std::vector<HostCallGraph> graphs;
+    const bool capturable = state && stream && mapped_v(h_features) && mapped_v(h_base_time);
     cudaGraphExec_t exec = nullptr;
     bool try_capture = false;
-    if (fresh) {
-        // new grid / network on this workspace: graphs captured for it carry
-        // stale kernel parameters (the fp32 head weights ride in them)
-        std::lock_guard<std::mutex> lock(graph_mu);
-        for (auto it = graphs.begin(); it != graphs.end();) {
-            if (it->key.ws == d_workspace) {
-                if (it->exec) cudaGraphExecDestroy(it->exec);
-                it = graphs.erase(it);
-            } else {
-                ++it;
+    HostCallGraph *entry = nullptr;
+    if (capturable) {
+        for (auto &g : state->graphs)
+            if (g.key == key2) entry = &g;
+        if (!entry) {
+            if (state->graphs.size() >= kMaxGraphsPerWorkspace) {
+                auto lru = state->graphs.begin();
+                for (auto it = state->graphs.begin(); it != state->graphs.end(); ++it)
+                    if (it->used < lru->used) lru = it;
+                if (lru->exec) cudaGraphExecDestroy(lru->exec);
+                state->graphs.erase(lru);
             }
+            state->graphs.push_back(HostCallGraph{key2});
+            entry = &state->graphs.back();
         }
-    } else {
-        std::lock_guard<std::mutex> lock(graph_mu);
-        for (auto &g : graphs)
-            if (g.key == key2) { if (g.exec) exec = g.exec; else if (++g.hits == 1) try_capture = true; }
-        if (!exec && !try_capture) { graphs.push_back(HostCallGraph{key2, nullptr, 0}); }
+        entry->used = ++state->clock;
+        if (entry->exec) exec = entry->exec;
+        else if (!entry->failed && ++entry->hits >= 2) try_capture = true;
     }
+    auto fail = [&](int code) {
+        if (state) state->key.clear();   // the workspace contents are unknown now
+        return code;
+    };
     if (exec) {
-        CS_TRY(cudaGraphLaunch(exec, st));
+        if (cudaGraphLaunch(exec, st) != cudaSuccess) { cudaGetLastError(); return fail(CS_ERR_CUDA); }
     } else if (try_capture) {
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t ge = nullptr;
@@ -1765,32 +1834,40 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
         if (ok) ok = cudaGraphInstantiate(&ge, graph, 0) == cudaSuccess;
         if (graph) cudaGraphDestroy(graph);
         cudaGetLastError();
-        {
-            std::lock_guard<std::mutex> lock(graph_mu);
-            for (auto &g : graphs)
-                if (g.key == key2) { g.exec = ok ? ge : nullptr; g.hits = ok ? 1 : 1 << 30; }
-        }
-        if (ok) CS_TRY(cudaGraphLaunch(ge, st));
-        else CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
-                                      h_weights, h_pairs, h_solo, h_clamps, h_counters, st));
+        entry->exec = ok ? ge : nullptr;
+        entry->failed = !ok;
+        int lrc = CS_OK;
+        if (ok) lrc = cudaGraphLaunch(ge, st) == cudaSuccess ? CS_OK : CS_ERR_CUDA;
+        else lrc = enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
+                                      h_weights, h_pairs, h_solo, h_clamps, h_counters, st);
+        if (lrc) { cudaGetLastError(); return fail(lrc); }
     } else {
-        CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws, L,
-                                 h_weights, h_pairs, h_solo, h_clamps, h_counters, st));
+        const int lrc = enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, rel_eps, ws,
+                                           L, h_weights, h_pairs, h_solo, h_clamps, h_counters, st);
+        if (lrc) return fail(lrc);
     }
-    CS_TRY(cudaStreamSynchronize(st));
+    if (cudaStreamSynchronize(st) != cudaSuccess) { cudaGetLastError(); return fail(CS_ERR_CUDA); }
+    if (fresh && state) state->key = key;
     // The screen's certain winners carry the observed fp32-vs-fp64 gap; argmin
     // parity needs it well inside rel_eps.  Otherwise (a network far outside
     // the trained range) redo the call with a wider ambiguity band -- more
     // pairs go to the exact fp64 resolve, the results stay identical.
+    uint32_t counters[2];
+    auto read_counters = [&]() -> bool {
+        if (h_counters) { memcpy(counters, h_counters, sizeof(counters)); return true; }
+        return cudaMemcpy(counters, ws + L.qcount, sizeof(counters), cudaMemcpyDeviceToHost) == cudaSuccess;
+    };
     for (double eps = rel_eps;;) {
+        if (!read_counters()) { cudaGetLastError(); return fail(CS_ERR_CUDA); }
         float err;
-        memcpy(&err, h_counters + 1, sizeof(err));
+        memcpy(&err, counters + 1, sizeof(err));
         if (!(err > 0.25 * eps)) break;
         eps = fmax(16.0 * eps, 16.0 * (double)err);
         if (!(eps < 0.1)) return CS_ERR_PRECISION;
-        CS_RC(enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, eps, ws, L,
-                                 h_weights, h_pairs, h_solo, h_clamps, h_counters, st));
-        CS_TRY(cudaStreamSynchronize(st));
+        const int lrc = enqueue_graph_call(net, h_grid, h_features, h_base_time, n_apps, eps, ws, L,
+                                           h_weights, h_pairs, h_solo, h_clamps, h_counters, st);
+        if (lrc) return fail(lrc);
+        if (cudaStreamSynchronize(st) != cudaSuccess) { cudaGetLastError(); return fail(CS_ERR_CUDA); }
     }
 #undef CS_TRY
 #undef CS_RC
@@ -1873,7 +1950,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
         if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
         if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
         if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
-        CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
+        if (h_counters) CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
     }
 #undef CS_TRY
 #undef CS_RC

@@ -15,6 +15,7 @@ size) launch kernels only:
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 from typing import Optional
 
@@ -198,6 +199,9 @@ class SweepPlan:
             ctypes.cast(_dptr(self.solo_split), nat.c_int32_p),
             ctypes.cast(_dptr(self.solo_clamps), nat.c_int32_p))
         self._side = torch.cuda.Stream(self.device)
+        # one sweep at a time through this plan's buffers: callers that share a
+        # cached plan (sweep.plan_for) hold it from launch to read-back
+        self.lock = threading.RLock()
         # the tcgen05 screen runs the fused pipeline: k_tables (+ solo
         # splits) -> k_sweep_tc3 (+ decide/scatter) -> k_resolve (+ decide);
         # the other screens keep tables | solo -> screen -> resolve -> decide
@@ -206,7 +210,7 @@ class SweepPlan:
 
     # ------------------------------------------------------------------
     def launch(self, d_features: torch.Tensor, d_base_time: torch.Tensor,
-               sweep_events: Optional[tuple] = None) -> None:
+               sweep_events: Optional[tuple] = None, rel_eps: Optional[float] = None) -> None:
         """Enqueue one full sweep on the current stream (no host sync).
 
         `sweep_events` = (start, end) CUDA events recorded around the k_sweep
@@ -220,6 +224,7 @@ class SweepPlan:
         if not (d_features.is_contiguous() and d_base_time.is_contiguous()):
             raise ValidationError("features and base_time must be contiguous")
         lib, dev = self.lib, self.device
+        eps = self.rel_eps if rel_eps is None else float(rel_eps)
         cur = torch.cuda.current_stream(dev)
         st = cur.cuda_stream
         self.counters.zero_()
@@ -238,7 +243,7 @@ class SweepPlan:
                 sweep_events[0].record(cur)
             nat.check(lib.cs_pair_screen_fused(
                 self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time), _dptr(self.solo_time),
-                _dptr(self.solo_clamps), self.pair_begin, self.pair_end, self.rel_eps,
+                _dptr(self.solo_clamps), self.pair_begin, self.pair_end, eps,
                 self.pair_out, _dptr(self.queue), cnt, _dptr(self.clamps), w, self.kernel_kind,
                 st), "cs_pair_screen_fused")
             if sweep_events is not None:
@@ -263,7 +268,7 @@ class SweepPlan:
         if sweep_events is not None:
             sweep_events[0].record(cur)
         nat.check(lib.cs_pair_screen(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
-                                     self.pair_begin, self.pair_end, self.rel_eps, self.pair_out,
+                                     self.pair_begin, self.pair_end, eps, self.pair_out,
                                      _dptr(self.queue), cnt, _dptr(self.clamps), self.kernel_kind,
                                      st), "cs_pair_screen")
         if sweep_events is not None:

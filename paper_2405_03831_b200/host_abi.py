@@ -63,6 +63,10 @@ class HostGraphCall:
             raise ValueError("cs_build_graph_workspace_bytes rejected the problem")
         self.ws = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
         self.ws_ptr = (self.ws.data_ptr() + 255) & ~255
+        # persistent workspace: grid / network / zeroed matrix stay resident and
+        # repeated calls replay as a CUDA graph; released in close()
+        nat.check(self.lib.cs_workspace_retain(self.ws_ptr, self.ws_bytes), "cs_workspace_retain")
+        self._retained = True
         self._t_feat, self.h_features = _pinned((n, 18), torch.float64)
         self._t_bt, self.h_base_time = _pinned((n,), torch.float64)
         self._t_w, self.h_weights = _pinned((L, n, n), torch.float64)
@@ -91,6 +95,18 @@ class HostGraphCall:
                       nat.ptr(self.h_base_time), self.n, self.rel_eps, self.ws_ptr, self.ws_bytes,
                       nat.ptr(self.h_weights), self.pairs, self.solo,
                       self.h_clamps.ctypes.data_as(nat.c_ull_p))
+
+    def close(self) -> None:
+        """Drop the workspace's library-side state (before its memory goes)."""
+        if getattr(self, "_retained", False):
+            self._retained = False
+            self.lib.cs_workspace_release(self.ws_ptr)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
     def bytes_per_call(self) -> tuple:
         """(H2D bytes, D2H bytes) moved by one repeated call (the grid and the
@@ -123,5 +139,8 @@ class HostGraphCall:
 
 def build_graph_host(weights, grid: KnobGrid, features, base_time, **kw) -> dict:
     call = HostGraphCall(weights, grid, len(base_time), **kw)
-    out = call(features, base_time)
-    return {k: np.array(v) for k, v in out.items()}
+    try:
+        out = call(features, base_time)
+        return {k: np.array(v) for k, v in out.items()}
+    finally:
+        call.close()

@@ -9,6 +9,7 @@ is the 2-job special case; ``scheduler.build_graph`` wraps the result in a
 
 from __future__ import annotations
 
+import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -23,17 +24,19 @@ from .grid import KnobGrid
 _PLAN_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
 _PLAN_CACHE_SIZE = 8
 _GRID_CACHE: "OrderedDict[tuple, KnobGrid]" = OrderedDict()
+_CACHE_LOCK = threading.RLock()     # the two caches are shared by caller threads
 
 
 def knob_grid(spaces: Sequence[ConfigSpace]) -> KnobGrid:
     key = tuple(spaces)
-    g = _GRID_CACHE.get(key)
-    if g is None:
-        g = KnobGrid(key)
-        _GRID_CACHE[key] = g
-        while len(_GRID_CACHE) > 32:
-            _GRID_CACHE.popitem(last=False)
-    return g
+    with _CACHE_LOCK:
+        g = _GRID_CACHE.get(key)
+        if g is None:
+            g = KnobGrid(key)
+            _GRID_CACHE[key] = g
+            while len(_GRID_CACHE) > 32:
+                _GRID_CACHE.popitem(last=False)
+        return g
 
 
 def plan_for(weights, spaces: Sequence[ConfigSpace], n: int, pair_begin: int = 0,
@@ -43,15 +46,16 @@ def plan_for(weights, spaces: Sequence[ConfigSpace], n: int, pair_begin: int = 0
     dev = require_cuda()
     key = (id(weights), tuple(spaces), n, pair_begin, pair_end, with_matrix, rel_eps, kernel,
            str(dev))
-    hit = _PLAN_CACHE.get(key)
-    if hit is not None and hit[0] is weights:
-        _PLAN_CACHE.move_to_end(key)
-        return hit[1]
-    plan = SweepPlan(weights, knob_grid(spaces), n, pair_begin, pair_end, dev,
-                     with_matrix=with_matrix, rel_eps=rel_eps, kernel=kernel)
-    _PLAN_CACHE[key] = (weights, plan)          # holds `weights` so its id stays unique
-    while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
-        _PLAN_CACHE.popitem(last=False)
+    with _CACHE_LOCK:
+        hit = _PLAN_CACHE.get(key)
+        if hit is not None and hit[0] is weights:
+            _PLAN_CACHE.move_to_end(key)
+            return hit[1]
+        plan = SweepPlan(weights, knob_grid(spaces), n, pair_begin, pair_end, dev,
+                         with_matrix=with_matrix, rel_eps=rel_eps, kernel=kernel)
+        _PLAN_CACHE[key] = (weights, plan)      # holds `weights` so its id stays unique
+        while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+            _PLAN_CACHE.popitem(last=False)
     return plan
 
 
@@ -93,32 +97,38 @@ def _inputs(jobs: Sequence[JobProfile]):
 
 def run_plan(plan: SweepPlan, features: np.ndarray, base_time: np.ndarray,
              with_matrix: bool = True) -> SweepResult:
-    d_f, d_b = to_device_inputs(features, base_time, plan.device)
-    with torch.cuda.device(plan.device):
-        plan.launch(d_f, d_b)
-        c = plan.read_counters()            # synchronizes the stream
-        # a network far outside the trained range: the fp32 screen's observed
-        # error is not well inside rel_eps -- widen the ambiguity band (more
-        # pairs go to the exact fp64 resolve; results identical) and redo
-        while c.screen_error > 0.25 * plan.rel_eps and 16.0 * plan.rel_eps < 0.1:
-            plan.rel_eps = min(max(16.0 * plan.rel_eps, 16.0 * c.screen_error), 0.099)
-            plan.launch(d_f, d_b)
-            c = plan.read_counters()
-        P = plan.P
-        res = SweepResult(
-            n=plan.n, grid=plan.grid, pair_begin=plan.pair_begin, pair_end=plan.pair_end,
-            corun_grid_index=plan.corun_grid_index[:, :P].cpu().numpy(),
-            corun_time=plan.corun_time[:, :P].cpu().numpy(),
-            corun_chosen=plan.corun_chosen[:, :P].cpu().numpy().astype(bool),
-            weight=plan.weight[:, :P].cpu().numpy(),
-            solo_time=plan.solo_time.cpu().numpy(),
-            solo_split=plan.solo_split.cpu().numpy(),
-            solo_clamps=plan.solo_clamps.cpu().numpy(),
-            clamps=c.clamps, queue_len=c.queue_len, screen_error=c.screen_error,
-            matrix=plan.matrix.cpu().numpy() if (with_matrix and plan.matrix is not None) else None)
-    if res.screen_error > 0.25 * plan.rel_eps:
+    """One sweep through `plan` and the host copies of its results.  Holds the
+    plan's lock from launch to read-back, so threads sharing a cached plan
+    (concurrent decide_pair / build_graph calls) never see each other's
+    buffers."""
+    with plan.lock:
+        d_f, d_b = to_device_inputs(features, base_time, plan.device)
+        eps = plan.rel_eps
+        with torch.cuda.device(plan.device):
+            plan.launch(d_f, d_b, rel_eps=eps)
+            c = plan.read_counters()            # synchronizes the stream
+            # a network far outside the trained range: the fp32 screen's observed
+            # error is not well inside rel_eps -- widen the ambiguity band (more
+            # pairs go to the exact fp64 resolve; results identical) and redo
+            while c.screen_error > 0.25 * eps and 16.0 * eps < 0.1:
+                eps = min(max(16.0 * eps, 16.0 * c.screen_error), 0.099)
+                plan.launch(d_f, d_b, rel_eps=eps)
+                c = plan.read_counters()
+            P = plan.P
+            res = SweepResult(
+                n=plan.n, grid=plan.grid, pair_begin=plan.pair_begin, pair_end=plan.pair_end,
+                corun_grid_index=plan.corun_grid_index[:, :P].cpu().numpy(),
+                corun_time=plan.corun_time[:, :P].cpu().numpy(),
+                corun_chosen=plan.corun_chosen[:, :P].cpu().numpy().astype(bool),
+                weight=plan.weight[:, :P].cpu().numpy(),
+                solo_time=plan.solo_time.cpu().numpy(),
+                solo_split=plan.solo_split.cpu().numpy(),
+                solo_clamps=plan.solo_clamps.cpu().numpy(),
+                clamps=c.clamps, queue_len=c.queue_len, screen_error=c.screen_error,
+                matrix=plan.matrix.cpu().numpy() if (with_matrix and plan.matrix is not None) else None)
+    if res.screen_error > 0.25 * eps:
         raise RuntimeError(f"fp32 screen error {res.screen_error:.3g} is too close to rel_eps "
-                           f"{plan.rel_eps:.3g}; argmin parity is no longer guaranteed")
+                           f"{eps:.3g}; argmin parity is no longer guaranteed")
     return res
 
 
