@@ -155,45 +155,66 @@ int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_a
 int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
             const double *d_base_time, cs_solo_out out, void *stream);
 
+/* Counters of one screen (cs_pair_screen[_fused] -> cs_resolve[_fused]);
+ * the caller zeroes them before each sweep (cs_prepare can). */
+typedef struct {
+    uint32_t queue_len;          /* (pair, budget)s queued for the exact fp64 re-scan        */
+    uint32_t screen_err_bits;    /* float bits: largest relative gap seen between a screened
+                                    time and its fp64 value (winners and near-tie runner-ups) */
+    uint32_t exact_rows;         /* (pair, member) rows queued for an fp64 re-count of their
+                                    floor clamps (a screened prediction within tau of 0.5)    */
+    uint32_t verify_fail;        /* sampled near-tie pairs whose exact fp64 re-scan disagreed
+                                    with the screen's winner (0 expected; the host redoes the
+                                    sweep with a wider band otherwise)                        */
+} cs_counters;
+
 /* cs_build_tables + cs_solo in ONE launch (each app's warp also evaluates its
  * exclusive splits; falls back to two launches when a grid stacks more than 32
- * solo splits).  Results identical to the two calls. */
+ * solo splits).  Results identical to the two calls.  d_counters and d_clamps
+ * (L x u64), when not NULL, are zeroed by the same launch -- ready for the
+ * screen that follows (no separate memsets in the sweep's CUDA graph). */
 int cs_prepare(const cs_network *net, const double *d_features, const double *d_base_time,
                int32_t n_apps, const cs_grid *d_grid, const cs_tables *tables, cs_solo_out out,
-               void *stream);
+               cs_counters *d_counters, unsigned long long *d_clamps, void *stream);
 
 /* The pair sweep is three stream-ordered steps (cs_solo may run concurrently
  * with the first two; only cs_pair_decide reads the solo results):
  *
  *   cs_pair_screen  screens every (pair, config) of the shard -- on the tensor
  *                   cores by default (CS_KERNEL_*) -- keeping per (pair,
- *                   budget) the first-index minimum and the runner-up.  When
- *                   the runner-up is more than rel_eps above the minimum the
- *                   winner is re-evaluated in fp64 (corun_grid_index /
- *                   corun_time final); otherwise corun_grid_index = -2 and the
- *                   (pair, budget) is appended to d_queue (needs L * P int64
- *                   slots).  d_queue_count holds two zeroed u32: [0] the queue
- *                   length, [1] the largest relative gap seen between a
- *                   screened winner and its fp64 value (float bits).  Co-run
- *                   floor clamps accumulate in d_clamps (L x u64, zeroed).
- *   cs_resolve      exact fp64 first-index argmin for every queued entry.
+ *                   budget) the first-index minimum and the runner-up (value
+ *                   and index).  When the runner-up is more than rel_eps above
+ *                   the minimum the winner is re-evaluated in fp64
+ *                   (corun_grid_index / corun_time final); a sample of the
+ *                   pairs whose runner-up is within 64 rel_eps is queued for a
+ *                   full fp64 re-scan as a check (d_counters->verify_fail).
+ *                   Ambiguous (pair, budget)s get
+ *                   corun_grid_index = -2 and an entry in d_queue, which needs
+ *                   (L + 2) * P int64 slots.  Co-run floor clamps accumulate
+ *                   in d_clamps (L x u64, zeroed): counted from the screen,
+ *                   except for a (pair, member) row with a screened
+ *                   prediction within tau = rel_eps / 2 of the 0.5 floor,
+ *                   which is queued (d_queue[L P ...], d_counters->exact_rows).
+ *   cs_resolve      exact fp64 first-index argmin for every queued (pair,
+ *                   budget); fp64 re-count of the floor clamps of every
+ *                   queued row into d_clamps.
  *   cs_pair_decide  co-run vs time-share per (pair, budget) against the solo
  *                   pair sum, adds the solo clamps the reference counts per
  *                   pair (so d_clamps ends equal to clamp_stats over
- *                   build_graph), and optionally scatters the winning times
- *                   into d_w (L x N x N, zeroed by the caller).
+ *                   build_graph, estimator.py:98-109), and optionally scatters
+ *                   the winning times into d_w (L x N x N, zeroed by the caller).
  *
  * `net` (host) is passed to the kernels that need it by value (parameter
  * bank).  cs_pair_sweep[_ex] = screen + resolve + decide without d_w. */
 int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                    const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-                   double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                   double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                    unsigned long long *d_clamps, int kernel_kind, void *stream);
 
 int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
-               void *stream);
+               cs_pair_out out, const int64_t *d_queue, cs_counters *d_counters,
+               unsigned long long *d_clamps, void *stream);
 
 int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32_t *d_solo_clamps,
                    int32_t n_apps, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
@@ -209,31 +230,31 @@ int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32
 int cs_pair_sweep_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                         const double *d_base_time, const double *d_solo_time,
                         const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                        double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                        double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                         unsigned long long *d_clamps, double *d_w, int kernel_kind, void *stream);
 /* Its two launches separately (cs_pair_sweep_fused = screen_fused + resolve_fused). */
 int cs_pair_screen_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                          const double *d_base_time, const double *d_solo_time,
                          const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
                          double rel_eps, cs_pair_out out, int64_t *d_queue,
-                         uint32_t *d_queue_count, unsigned long long *d_clamps, double *d_w,
+                         cs_counters *d_counters, unsigned long long *d_clamps, double *d_w,
                          int kernel_kind, void *stream);
 int cs_resolve_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, const double *d_solo_time,
                      const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                     cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+                     cs_pair_out out, const int64_t *d_queue, cs_counters *d_counters,
                      unsigned long long *d_clamps, double *d_w, void *stream);
 
 int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                   const double *d_base_time, const double *d_solo_time,
                   const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                  double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                  double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                   unsigned long long *d_clamps, void *stream);
 
 int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, const double *d_solo_time,
                      const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                      unsigned long long *d_clamps, int kernel_kind, void *stream);
 
 /* W[i*N+j] = W[j*N+i] = weight of budget `budget`; the caller zeroes W. */

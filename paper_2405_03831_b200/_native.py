@@ -70,6 +70,10 @@ class CsSoloOut(ctypes.Structure):
     _fields_ = [("solo_time", c_double_p), ("solo_split", c_int32_p), ("solo_clamps", c_int32_p)]
 
 
+# cs_counters (include/cosched_b200.h): 4 u32
+COUNTERS_BYTES = 4 * 4
+
+
 SWEEP_SYMBOLS = {
     # name: (restype, argtypes)
     "cs_version": (ctypes.c_char_p, []),
@@ -84,7 +88,7 @@ SWEEP_SYMBOLS = {
                                              ctypes.c_void_p]),
     "cs_prepare": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_int32, ctypes.POINTER(CsGrid), ctypes.POINTER(CsTables),
-                                  CsSoloOut, ctypes.c_void_p]),
+                                  CsSoloOut, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_solo": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
                                ctypes.POINTER(CsGrid), ctypes.c_void_p, CsSoloOut, ctypes.c_void_p]),
     "cs_pair_sweep": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
@@ -123,7 +127,7 @@ SWEEP_SYMBOLS = {
     "cs_resolve": (ctypes.c_int, [ctypes.POINTER(CsNetwork), ctypes.POINTER(CsTables),
                                   ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_int64, CsPairOut, ctypes.c_void_p, ctypes.c_void_p,
-                                  ctypes.c_void_p]),
+                                  ctypes.c_void_p, ctypes.c_void_p]),
     "cs_pair_decide": (ctypes.c_int, [ctypes.POINTER(CsGrid), ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, CsPairOut,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),

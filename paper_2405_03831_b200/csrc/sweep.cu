@@ -270,6 +270,14 @@ __device__ __forceinline__ double member_time64_lean(const cs_tables &t, const H
     return (y < FLOOR ? FLOOR : y) * __ldg(base_time + self);
 }
 
+// fp64 floor test of one member's prediction (estimator.py:106-109): 1 if clamped
+__device__ __forceinline__ int member_floor64(const cs_tables &t, const Head64P &net, int self,
+                                              int other, int c, int member) {
+    double z[HD];
+    z64_row(t, self, other, c, member, z);
+    return head64_lean(net, z) < FLOOR ? 1 : 0;
+}
+
 // CoRunTime of one config for pair (i, j): max over members (estimator.py:127-129)
 __device__ __forceinline__ double corun64(const cs_tables &t, const Head64P &net,
                                           const double *w2t,
@@ -292,10 +300,15 @@ struct SweepArgs {
     const int32_t *solo_clamps;
     int32_t n, log2s;
     int64_t p_begin, P;
-    float eps;
+    float eps;               // ambiguity band: runner-up within eps -> exact re-scan
+    float near;              // runner-up within near (> eps): a sample of these pairs is
+    int64_t vstride;         // (every vstride-th pair) fully re-scanned by k_resolve
+    float tau;               // a row with a prediction within tau of the 0.5 floor
+                             // has its floor clamps re-counted in fp64
     cs_pair_out out;
-    int64_t *queue;
-    uint32_t *qcount;
+    int64_t *queue;          // (L + 2) P slots: [0, L P) re-scan / verify queue, then
+                             // the queue of rows whose clamps k_resolve re-counts
+    cs_counters *cnt;
     unsigned long long *clamps;
     uint32_t *trace;         // debug builds (CS_TC_TRACE): per-thread progress, host-mapped
     // fused tail (k_sweep_tc3 via cs_pair_sweep_fused): ambiguous pairs are
@@ -308,13 +321,40 @@ struct SweepArgs {
 __device__ __forceinline__ bool screen_ambiguous(const SweepArgs &a, float best, float second) {
     return !(second > best * (1.0f + a.eps));
 }
+// non-ambiguous but close: the runner-up gets an fp64 re-evaluation as well
+__device__ __forceinline__ bool screen_near(const SweepArgs &a, float best, float second) {
+    return !(second > best * (1.0f + a.near));
+}
 
 // ambiguous (pair, budget): leave it to k_resolve
 __device__ __forceinline__ void push_ambiguous(const SweepArgs &a, int l, int64_t pl) {
     const int64_t o = (int64_t)l * a.P + pl;
     a.out.corun_grid_index[o] = CS_SCREEN_AMBIGUOUS;
-    const uint32_t q = atomicAdd(a.qcount, 1u);
+    const uint32_t q = atomicAdd(&a.cnt->queue_len, 1u);
     a.queue[q] = (pl << 4) | l;
+}
+
+// a (pair, member) row with a screened prediction within tau of the floor:
+// k_resolve re-counts its clamps in fp64 (the screen does not count them)
+__device__ __forceinline__ void push_row(const SweepArgs &a, int64_t pl, int member) {
+    const uint32_t q = atomicAdd(&a.cnt->exact_rows, 1u);
+    a.queue[(int64_t)a.g.L * a.P + q] = (pl << 1) | member;
+}
+
+// a certain winner whose runner-up is near (eps < gap <= near): every
+// vstride-th such pair is re-scanned in fp64 by k_resolve as a check of the
+// screen's order (a disagreement flags the sweep; the host then redoes it
+// with a wider band).  Entries share the re-scan queue, tagged by bit 3.
+__device__ __forceinline__ void maybe_verify(const SweepArgs &a, int l, int64_t pl, float best,
+                                             float second) {
+    if (!screen_near(a, best, second) || (a.p_begin + pl) % a.vstride) return;
+    const uint32_t q = atomicAdd(&a.cnt->queue_len, 1u);
+    a.queue[q] = (pl << 4) | 8 | l;
+}
+
+// the screen-error monitor: relative gap between a screened time and its fp64 value
+__device__ __forceinline__ void monitor(const SweepArgs &a, double exact, float screened) {
+    atomicMax(&a.cnt->screen_err_bits, __float_as_uint((float)(fabs(exact - (double)screened) / exact)));
 }
 
 // certain winner: its exact fp64 CoRunTime (+ the screen-error monitor)
@@ -323,7 +363,7 @@ __device__ __forceinline__ void write_winner(const SweepArgs &a, int l, int64_t 
     const int64_t o = (int64_t)l * a.P + pl;
     a.out.corun_grid_index[o] = idx;
     a.out.corun_time[o] = co;
-    atomicMax(a.qcount + 1, __float_as_uint((float)(fabs(co - (double)best) / co)));
+    monitor(a, co, best);
 }
 
 // co-run vs time-share for one (pair, budget) (hwopt.py:77-87) with the solo
@@ -423,7 +463,9 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
                                                 const double *__restrict__ feats, int n,
                                                 const GridP g, const cs_tables t,
                                                 const double *__restrict__ base_time,
-                                                cs_solo_out solo, int do_solo) {
+                                                cs_solo_out solo, int do_solo,
+                                                cs_counters *reset_cnt,
+                                                unsigned long long *reset_clamps) {
     __shared__ TablesSmem sm;
     // let a programmatically dependent sweep start its prologue now (it still
     // waits for this grid to finish before reading the tables)
@@ -442,6 +484,12 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
     }
     // the image predates the previous kernel; the features may come from it
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // fresh counters for the screen (it reads them only after this grid completes)
+    if (blockIdx.x == 0) {
+        if (reset_cnt && threadIdx.x < (int)(sizeof(cs_counters) / 4))
+            reinterpret_cast<uint32_t *>(reset_cnt)[threadIdx.x] = 0u;
+        if (reset_clamps && threadIdx.x < g.L) reset_clamps[threadIdx.x] = 0ull;
+    }
     __syncthreads();
     const Net64P &net = sm.net;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -580,6 +628,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
     int idx[L], clamps[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; clamps[l] = 0; }
+    float mind = FLT_MAX;     // closest screened prediction to the 0.5 floor
 
     if (live) {
         float p1[HD], p2[HD], tmp[HD];
@@ -605,6 +654,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
             for (int h = 0; h < HD; ++h) z[h] += p2[h];
             const float y2 = head32(net, z);
             const int cl = (y1 < 0.5f) + (y2 < 0.5f);
+            mind = fminf(mind, fminf(fabsf(y1 - 0.5f), fabsf(y2 - 0.5f)));
             const float tt = fmaxf(fmaxf(y1, 0.5f) * ti, fmaxf(y2, 0.5f) * tj);
 #pragma unroll
             for (int l = 0; l < L; ++l) {
@@ -617,15 +667,29 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
         }
     }
 
+    // a prediction too close to the floor for the screen to count its clamp:
+    // k_resolve re-counts the pair's rows in fp64 (every slice of the pair
+    // drops its screened count; slice 0 queues both members)
+    {
+        // the pair's slices are adjacent lanes: OR their flags
+        int f = live && mind <= a.tau;
+        for (int off = 1; off < S; off <<= 1) f |= __shfl_xor_sync(0xffffffffu, f, off);
+        if (f) {
+#pragma unroll
+            for (int l = 0; l < L; ++l) clamps[l] = 0;
+            if (s == 0) { push_row(a, pl, 0); push_row(a, pl, 1); }
+        }
+    }
+
     // merge the S slices of a pair (adjacent lanes): lexicographic (value, index)
 #pragma unroll
     for (int l = 0; l < L; ++l) {
         for (int off = 1; off < S; off <<= 1) {
-            float ob = __shfl_xor_sync(0xffffffffu, best[l], off);
-            float os = __shfl_xor_sync(0xffffffffu, second[l], off);
-            int oi = __shfl_xor_sync(0xffffffffu, idx[l], off);
-            bool other = ob < best[l] || (ob == best[l] && oi < idx[l]);
-            float loser = other ? best[l] : ob;
+            const float ob = __shfl_xor_sync(0xffffffffu, best[l], off);
+            const float os = __shfl_xor_sync(0xffffffffu, second[l], off);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx[l], off);
+            const bool other = ob < best[l] || (ob == best[l] && oi < idx[l]);
+            const float loser = other ? best[l] : ob;
             second[l] = fminf(fminf(second[l], os), loser);
             if (other) { best[l] = ob; idx[l] = oi; }
         }
@@ -640,6 +704,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
         const double co = fmax(member_time64_lean(a.t, net64, a.base_time, i, j, idx[l], 0),
                                member_time64_lean(a.t, net64, a.base_time, j, i, idx[l], 1));
         write_winner(a, l, pl, idx[l], co, best[l]);
+        maybe_verify(a, l, pl, best[l], second[l]);
     }
 }
 
@@ -652,7 +717,7 @@ struct ResolveArgs {
     int64_t p_begin, P;
     cs_pair_out out;
     const int64_t *queue;
-    const uint32_t *qcount;
+    cs_counters *cnt;
     // fused (cs_pair_sweep_fused): also decide + scatter each resolved entry
     int fused;
     const int32_t *solo_clamps;
@@ -662,8 +727,9 @@ struct ResolveArgs {
 
 __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
                                                  const __grid_constant__ Head64P net_param) {
-    // One block per queued (pair, budget); thread c evaluates configs c, c+128, ...
-    // in fp64, then a block-wide first-index argmin (ties -> smallest index).
+    // One block per queued (pair, budget); thread c evaluates configs c,
+    // c+128, ... in fp64, then a block-wide first-index argmin (ties ->
+    // smallest index).
     __shared__ Head64P net_sm;
     __shared__ double red_v[4];
     __shared__ int red_i[4];
@@ -674,14 +740,15 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
         w2t[q] = __ldg(a.t.net_image + kImgHeadOff + (q % HD) * HD + q / HD);
     const Head64P &net64 = stage_head64(a.t.net_image, net_sm);   // (its __syncthreads covers w2t)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    // blocks past the (device-side) queue length leave
-    const uint32_t count = *a.qcount;
-    if (blockIdx.x >= count) return;
+    // blocks past both (device-side) queue lengths leave
+    const uint32_t count = a.cnt->queue_len, rows = a.cnt->exact_rows;
+    if (blockIdx.x >= count && blockIdx.x >= rows) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t q = blockIdx.x; q < count; q += gridDim.x) {
         const int64_t e = a.queue[q];
         const int64_t pl = e >> 4;
-        const int l = (int)(e & 15);
+        const int l = (int)(e & 7);
+        const bool verify = (e & 8) != 0;   // a certain winner re-scanned as a check
         int i, j;
         pair_of(a.p_begin + pl, a.n, i, j);
         double best = INFINITY;
@@ -702,6 +769,11 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
             for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
                 if (red_v[w] < best || (red_v[w] == best && red_i[w] < arg)) { best = red_v[w]; arg = red_i[w]; }
             const int64_t o = (int64_t)l * a.P + pl;
+            if (verify) {
+                // the screen's winner (index and fp64 time) must be the exact one
+                if (a.out.corun_grid_index[o] != arg || a.out.corun_time[o] != best)
+                    atomicAdd(&a.cnt->verify_fail, 1u);
+            } else {
             a.out.corun_grid_index[o] = arg == INT_MAX ? -1 : arg;
             a.out.corun_time[o] = arg == INT_MAX ? INFINITY : best;
             if (a.fused) {
@@ -709,6 +781,38 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
                                             arg == INT_MAX ? INFINITY : best);
                 if (cl) atomicAdd(a.clamps + l, (unsigned long long)cl);
             }
+            }
+        }
+        __syncthreads();
+    }
+    // rows whose floor clamps the screen could not count: all their co-run
+    // predictions re-counted in fp64 (estimator.py:106-109)
+    __shared__ unsigned int red_c[4][CS_MAX_BUDGETS];
+    for (int64_t q = blockIdx.x; q < rows; q += gridDim.x) {
+        const int64_t e = a.queue[(int64_t)a.g.L * a.P + q];
+        const int64_t pl = e >> 1;
+        const int member = (int)(e & 1);
+        int i, j;
+        pair_of(a.p_begin + pl, a.n, i, j);
+        unsigned int cl[CS_MAX_BUDGETS] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c = threadIdx.x; c < a.g.G; c += blockDim.x) {
+            double z[HD];
+            z64_row(a.t, member ? j : i, member ? i : j, c, member, z);
+            if (head64t(net64, w2t, z) < FLOOR) {
+                const uint32_t m = __ldg(a.g.mask + c);
+#pragma unroll
+                for (int l = 0; l < CS_MAX_BUDGETS; ++l) cl[l] += (m >> l) & 1u;
+            }
+        }
+        for (int l = 0; l < a.g.L; ++l) {
+            const unsigned int v = __reduce_add_sync(0xffffffffu, cl[l]);
+            if (lane == 0) red_c[warp][l] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < a.g.L) {
+            unsigned long long v = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red_c[w][threadIdx.x];
+            if (v) atomicAdd(a.clamps + threadIdx.x, v);
         }
         __syncthreads();
     }
@@ -936,7 +1040,9 @@ int check_launch() {
 }
 
 int check_grid(const cs_grid *g) {
-    if (!g || g->n_grid < 0 || g->n_budgets < 1 || g->n_budgets > CS_MAX_BUDGETS) return CS_ERR_ARG;
+    // (a config index fits 13 bits of a clamp-queue entry)
+    if (!g || g->n_grid < 0 || g->n_grid >= 8192 || g->n_budgets < 1 || g->n_budgets > CS_MAX_BUDGETS)
+        return CS_ERR_ARG;
     if (g->n_grid > 0 && (!g->knob1 || !g->knob2 || !g->mask)) return CS_ERR_ARG;
     // Empty budgets are legal here (the reference's optimize_corun works on a
     // budget without solo splits and optimize_solo_pair on one without co-run
@@ -1092,7 +1198,8 @@ int cs_tables_set_network(const cs_network *net, const cs_tables *tables, void *
 namespace {
 int launch_tables(const cs_network *net, const double *d_features, int32_t n_apps,
                   const cs_grid *d_grid, const cs_tables *tables, const double *d_base_time,
-                  cs_solo_out solo, int do_solo, void *stream) {
+                  cs_solo_out solo, int do_solo, cs_counters *reset_cnt,
+                  unsigned long long *reset_clamps, void *stream) {
     Net64P np;
     if (!net64_from(net, &np) || !tables || n_apps < 2 || !d_features) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
@@ -1115,10 +1222,11 @@ int launch_tables(const cs_network *net, const double *d_features, int32_t n_app
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, k_tables, np, d_features, n_apps, g, *tables, d_base_time, solo,
-                           do_solo) != cudaSuccess) {
+                           do_solo, reset_cnt, reset_clamps) != cudaSuccess) {
         cudaGetLastError();
         k_tables<<<blocks, 128, 0, (cudaStream_t)stream>>>(np, d_features, n_apps, g, *tables,
-                                                            d_base_time, solo, do_solo);
+                                                            d_base_time, solo, do_solo, reset_cnt,
+                                                            reset_clamps);
     }
     return check_launch();
 }
@@ -1126,19 +1234,22 @@ int launch_tables(const cs_network *net, const double *d_features, int32_t n_app
 
 int cs_build_tables(const cs_network *net, const double *d_features, int32_t n_apps,
                     const cs_grid *d_grid, const cs_tables *tables, void *stream) {
-    return launch_tables(net, d_features, n_apps, d_grid, tables, nullptr, cs_solo_out{}, 0, stream);
+    return launch_tables(net, d_features, n_apps, d_grid, tables, nullptr, cs_solo_out{}, 0, nullptr,
+                         nullptr, stream);
 }
 
 int cs_prepare(const cs_network *net, const double *d_features, const double *d_base_time,
                int32_t n_apps, const cs_grid *d_grid, const cs_tables *tables, cs_solo_out out,
-               void *stream) {
+               cs_counters *d_counters, unsigned long long *d_clamps, void *stream) {
     int rc = check_grid(d_grid);
     if (rc) return rc;
     if (!d_base_time || !out.solo_time || !out.solo_split) return CS_ERR_ARG;
     const int S = d_grid->solo_offsets[d_grid->n_budgets];
     if (S <= 32)   // one warp per app evaluates all its splits
-        return launch_tables(net, d_features, n_apps, d_grid, tables, d_base_time, out, 1, stream);
-    rc = launch_tables(net, d_features, n_apps, d_grid, tables, nullptr, cs_solo_out{}, 0, stream);
+        return launch_tables(net, d_features, n_apps, d_grid, tables, d_base_time, out, 1, d_counters,
+                             d_clamps, stream);
+    rc = launch_tables(net, d_features, n_apps, d_grid, tables, nullptr, cs_solo_out{}, 0, d_counters,
+                       d_clamps, stream);
     if (rc) return rc;
     return cs_solo(net, tables, d_grid, d_base_time, out, stream);
 }
@@ -1160,24 +1271,24 @@ int cs_solo(const cs_network *net, const cs_tables *tables, const cs_grid *d_gri
 namespace {
 int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                      unsigned long long *d_clamps, int kernel_kind, const double *d_solo_time,
                      const int32_t *d_solo_clamps, double *d_w, int fused, void *stream);
 }
 
 int cs_pair_screen(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                    const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-                   double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                   double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                    unsigned long long *d_clamps, int kernel_kind, void *stream) {
     return pair_screen_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
-                            d_queue, d_queue_count, d_clamps, kernel_kind, nullptr, nullptr,
+                            d_queue, d_counters, d_clamps, kernel_kind, nullptr, nullptr,
                             nullptr, 0, stream);
 }
 
 namespace {
 int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                  const double *d_base_time, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
-                 const int64_t *d_queue, const uint32_t *d_queue_count, const double *d_solo_time,
+                 const int64_t *d_queue, cs_counters *d_counters, const double *d_solo_time,
                  const int32_t *d_solo_clamps, unsigned long long *d_clamps, double *d_w,
                  int fused, void *stream);
 }
@@ -1186,24 +1297,24 @@ int cs_pair_screen_fused(const cs_network *net, const cs_tables *tables, const c
                          const double *d_base_time, const double *d_solo_time,
                          const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
                          double rel_eps, cs_pair_out out, int64_t *d_queue,
-                         uint32_t *d_queue_count, unsigned long long *d_clamps, double *d_w,
+                         cs_counters *d_counters, unsigned long long *d_clamps, double *d_w,
                          int kernel_kind, void *stream) {
     if (!d_solo_time || !out.corun_chosen || !out.weight || !d_queue) return CS_ERR_ARG;
     if (kernel_kind == CS_KERNEL_AUTO) kernel_kind = CS_KERNEL_TCGEN05;
     if (kernel_kind != CS_KERNEL_TCGEN05 && (kernel_kind & 0xF00) != 0x300) return CS_ERR_ARG;
     return pair_screen_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
-                            d_queue, d_queue_count, d_clamps, kernel_kind, d_solo_time,
+                            d_queue, d_counters, d_clamps, kernel_kind, d_solo_time,
                             d_solo_clamps, d_w, 1, stream);
 }
 
 int cs_resolve_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, const double *d_solo_time,
                      const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                     cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
+                     cs_pair_out out, const int64_t *d_queue, cs_counters *d_counters,
                      unsigned long long *d_clamps, double *d_w, void *stream) {
     if (!d_solo_time || !out.corun_chosen || !out.weight || !d_clamps) return CS_ERR_ARG;
     return resolve_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
-                        d_queue_count, d_solo_time, d_solo_clamps, d_clamps, d_w, 1, stream);
+                        d_counters, d_solo_time, d_solo_clamps, d_clamps, d_w, 1, stream);
 }
 
 namespace {
@@ -1226,33 +1337,33 @@ bool fp16_screen_safe(const cs_network *net) {
 int cs_pair_sweep_fused(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                         const double *d_base_time, const double *d_solo_time,
                         const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                        double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                        double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                         unsigned long long *d_clamps, double *d_w, int kernel_kind, void *stream) {
     if (kernel_kind == CS_KERNEL_AUTO && !fp16_screen_safe(net)) {
         // beyond the fp16 range: the fp32 SIMT screen, then resolve + decide
         // (+ scatter) as separate steps -- identical results
         int rc = cs_pair_screen(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps,
-                                out, d_queue, d_queue_count, d_clamps, CS_KERNEL_SIMT, stream);
+                                out, d_queue, d_counters, d_clamps, CS_KERNEL_SIMT, stream);
         if (rc) return rc;
         rc = cs_resolve(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
-                        d_queue_count, stream);
+                        d_counters, d_clamps, stream);
         if (rc) return rc;
         return cs_pair_decide(d_grid, d_solo_time, d_solo_clamps, tables->n_apps, pair_begin,
                               pair_end, out, d_clamps, d_w, stream);
     }
     int rc = cs_pair_screen_fused(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
-                                  pair_begin, pair_end, rel_eps, out, d_queue, d_queue_count,
+                                  pair_begin, pair_end, rel_eps, out, d_queue, d_counters,
                                   d_clamps, d_w, kernel_kind, stream);
     if (rc) return rc;
     return cs_resolve_fused(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
-                            pair_begin, pair_end, out, d_queue, d_queue_count, d_clamps, d_w,
+                            pair_begin, pair_end, out, d_queue, d_counters, d_clamps, d_w,
                             stream);
 }
 
 namespace {
 int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                      unsigned long long *d_clamps, int kernel_kind, const double *d_solo_time,
                      const int32_t *d_solo_clamps, double *d_w, int fused, void *stream) {
     Net64P n64;
@@ -1260,7 +1371,7 @@ int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_gr
     int rc = check_grid(d_grid);
     if (rc) return rc;
     if (!tables || !d_base_time || !d_clamps || !out.corun_grid_index || !out.corun_time ||
-        !d_queue || !d_queue_count)
+        !d_queue || !d_counters)
         return CS_ERR_ARG;
     const int64_t n = tables->n_apps;
     const int64_t P_all = n * (n - 1) / 2;
@@ -1282,9 +1393,14 @@ int pair_screen_impl(const cs_network *net, const cs_tables *tables, const cs_gr
     a.P = pair_end - pair_begin;
     a.log2s = choose_log2_slices(a.P, a.g.G);
     a.eps = (float)rel_eps;
+    a.near = (float)fmin(64.0 * rel_eps, 0.05);
+    // verify ~1/8 of the near pairs, at most a few hundred per sweep (one wave
+    // of k_resolve blocks)
+    a.vstride = a.P >> 14 > 8 ? a.P >> 14 : 8;
+    a.tau = (float)(0.5 * rel_eps);
     a.out = out;
     a.queue = d_queue;
-    a.qcount = d_queue_count;
+    a.cnt = d_counters;
     a.clamps = d_clamps;
     a.trace = nullptr;
     a.fused = fused;
@@ -1360,23 +1476,23 @@ int cs_pair_decide(const cs_grid *d_grid, const double *d_solo_time, const int32
 int cs_pair_sweep(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                   const double *d_base_time, const double *d_solo_time,
                   const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                  double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                  double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                   unsigned long long *d_clamps, void *stream) {
     return cs_pair_sweep_ex(net, tables, d_grid, d_base_time, d_solo_time, d_solo_clamps,
-                            pair_begin, pair_end, rel_eps, out, d_queue, d_queue_count, d_clamps,
+                            pair_begin, pair_end, rel_eps, out, d_queue, d_counters, d_clamps,
                             CS_KERNEL_AUTO, stream);
 }
 
 int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                      const double *d_base_time, const double *d_solo_time,
                      const int32_t *d_solo_clamps, int64_t pair_begin, int64_t pair_end,
-                     double rel_eps, cs_pair_out out, int64_t *d_queue, uint32_t *d_queue_count,
+                     double rel_eps, cs_pair_out out, int64_t *d_queue, cs_counters *d_counters,
                      unsigned long long *d_clamps, int kernel_kind, void *stream) {
     int rc = cs_pair_screen(net, tables, d_grid, d_base_time, pair_begin, pair_end, rel_eps, out,
-                            d_queue, d_queue_count, d_clamps, kernel_kind, stream);
+                            d_queue, d_counters, d_clamps, kernel_kind, stream);
     if (rc) return rc;
     rc = cs_resolve(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
-                    d_queue_count, stream);
+                    d_counters, d_clamps, stream);
     if (rc) return rc;
     return cs_pair_decide(d_grid, d_solo_time, d_solo_clamps, tables->n_apps, pair_begin,
                           pair_end, out, d_clamps, nullptr, stream);
@@ -1385,14 +1501,14 @@ int cs_pair_sweep_ex(const cs_network *net, const cs_tables *tables, const cs_gr
 namespace {
 int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                  const double *d_base_time, int64_t pair_begin, int64_t pair_end, cs_pair_out out,
-                 const int64_t *d_queue, const uint32_t *d_queue_count, const double *d_solo_time,
+                 const int64_t *d_queue, cs_counters *d_counters, const double *d_solo_time,
                  const int32_t *d_solo_clamps, unsigned long long *d_clamps, double *d_w,
                  int fused, void *stream) {
     Net64P n64;
     if (!net64_from(net, &n64)) return CS_ERR_ARG;
     int rc = check_grid(d_grid);
     if (rc) return rc;
-    if (!tables || !d_base_time || !d_queue || !d_queue_count) return CS_ERR_ARG;
+    if (!tables || !d_base_time || !d_queue || !d_counters) return CS_ERR_ARG;
     if (pair_begin == pair_end) return CS_OK;
     ResolveArgs a{};
     a.t = *tables;
@@ -1403,7 +1519,7 @@ int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *
     a.P = pair_end - pair_begin;
     a.out = out;
     a.queue = d_queue;
-    a.qcount = d_queue_count;
+    a.cnt = d_counters;
     a.fused = fused;
     a.solo_time = d_solo_time;
     a.solo_clamps = d_solo_clamps;
@@ -1432,10 +1548,11 @@ int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *
 
 int cs_resolve(const cs_network *net, const cs_tables *tables, const cs_grid *d_grid,
                const double *d_base_time, int64_t pair_begin, int64_t pair_end,
-               cs_pair_out out, const int64_t *d_queue, const uint32_t *d_queue_count,
-               void *stream) {
+               cs_pair_out out, const int64_t *d_queue, cs_counters *d_counters,
+               unsigned long long *d_clamps, void *stream) {
+    if (!d_clamps) return CS_ERR_ARG;
     return resolve_impl(net, tables, d_grid, d_base_time, pair_begin, pair_end, out, d_queue,
-                        d_queue_count, nullptr, nullptr, nullptr, nullptr, 0, stream);
+                        d_counters, nullptr, nullptr, d_clamps, nullptr, 0, stream);
 }
 
 int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begin,
@@ -1544,8 +1661,8 @@ GraphLayout graph_layout(int32_t n, const cs_grid *g) {
     L.corun_time = put(sizeof(double) * (size_t)(nb * P));
     L.chosen = put(sizeof(uint8_t) * (size_t)(nb * P));
     L.weight = put(sizeof(double) * (size_t)(nb * P));
-    L.queue = put(sizeof(int64_t) * (size_t)(nb * P));
-    L.qcount = put(sizeof(uint32_t) * 2);
+    L.queue = put(sizeof(int64_t) * (size_t)((nb + 2) * P));
+    L.qcount = put(sizeof(cs_counters));
     L.clamps = put(sizeof(unsigned long long) * (size_t)nb);
     L.W = put(sizeof(double) * (size_t)n * n * nb);
     L.total = off;
@@ -1578,18 +1695,16 @@ size_t cs_build_graph_workspace_bytes(int32_t n_apps, const cs_grid *h_grid) {
 
 namespace {
 // Host-call prologue when the caller's inputs sit in pinned (device-mapped)
-// memory: read them over PCIe straight into the workspace and zero the
-// queue / clamp counters -- one launch instead of two H2D copies + a memset.
+// memory: read them over PCIe straight into the workspace -- one launch
+// instead of two H2D copies.
 __global__ void k_call_begin(const double *__restrict__ hf, const double *__restrict__ hbt,
-                             double *__restrict__ df, double *__restrict__ dbt, int n,
-                             uint32_t *__restrict__ zero, int zero_words) {
+                             double *__restrict__ df, double *__restrict__ dbt, int n) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // k_tables may stage now
-    const int64_t nf = (int64_t)n * NF, total = nf + n + zero_words;
+    const int64_t nf = (int64_t)n * NF, total = nf + n;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
         if (k < nf) df[k] = hf[k];
-        else if (k < nf + n) dbt[k - nf] = hbt[k - nf];
-        else zero[k - nf - n] = 0u;
+        else dbt[k - nf] = hbt[k - nf];
     }
 }
 
@@ -1608,7 +1723,7 @@ struct CallEndArgs {
     int nb;
 };
 __global__ void k_call_end(const CallEndArgs a) {
-    const int64_t total = 3 * a.LN + a.nb + 2;
+    const int64_t total = 3 * a.LN + a.nb + 4;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
         if (k < a.LN) { if (a.h_solo_time) a.h_solo_time[k] = a.solo_time[k]; }
@@ -1678,7 +1793,7 @@ int cs_workspace_retain(void *d_workspace, size_t workspace_bytes) {
     if (!d_workspace || ((uintptr_t)d_workspace & 255) || !workspace_bytes) return CS_ERR_ARG;
     auto st = std::make_shared<WorkspaceState>();
     st->bytes = workspace_bytes;
-    if (cudaHostAlloc((void **)&st->h_counters, sizeof(uint32_t) * 2, cudaHostAllocDefault) !=
+    if (cudaHostAlloc((void **)&st->h_counters, sizeof(cs_counters), cudaHostAllocDefault) !=
         cudaSuccess) {
         cudaGetLastError();
         return CS_ERR_CUDA;
@@ -1852,15 +1967,18 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
     // parity needs it well inside rel_eps.  Otherwise (a network far outside
     // the trained range) redo the call with a wider ambiguity band -- more
     // pairs go to the exact fp64 resolve, the results stay identical.
-    uint32_t counters[2];
+    cs_counters counters;
     auto read_counters = [&]() -> bool {
-        if (h_counters) { memcpy(counters, h_counters, sizeof(counters)); return true; }
-        return cudaMemcpy(counters, ws + L.qcount, sizeof(counters), cudaMemcpyDeviceToHost) == cudaSuccess;
+        if (h_counters) { memcpy(&counters, h_counters, sizeof(counters)); return true; }
+        return cudaMemcpy(&counters, ws + L.qcount, sizeof(counters), cudaMemcpyDeviceToHost) == cudaSuccess;
     };
     for (double eps = rel_eps;;) {
         if (!read_counters()) { cudaGetLastError(); return fail(CS_ERR_CUDA); }
         float err;
-        memcpy(&err, counters + 1, sizeof(err));
+        memcpy(&err, &counters.screen_err_bits, sizeof(err));
+        // a sampled exact re-scan disagreeing with the screen counts like an
+        // error at the band itself
+        if (counters.verify_fail) err = fmaxf(err, (float)eps);
         if (!(err > 0.25 * eps)) break;
         eps = fmax(16.0 * eps, 16.0 * (double)err);
         if (!(eps < 0.1)) return CS_ERR_PRECISION;
@@ -1887,20 +2005,18 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
 #define CS_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { \
         fprintf(stderr, "cosched_b200: %s\n", cudaGetErrorString(_e)); return CS_ERR_CUDA; } } while (0)
 #define CS_RC(x) do { int _r = (x); if (_r) return _r; } while (0)
-    // queue counters and clamp counters are adjacent: zeroed together
-    const size_t zero_bytes = (L.clamps - L.qcount) + sizeof(unsigned long long) * nb;
+    // (the queue / clamp counters are zeroed by k_tables, cs_prepare below)
     const double *zf = (const double *)mapped_v(h_features), *zb = (const double *)mapped_v(h_base_time);
     if (zf && zb) {
-        const int64_t items = (int64_t)n * NF + n + (int64_t)(zero_bytes / 4);
+        const int64_t items = (int64_t)n * NF + n;
         int blocks = (int)((items + 255) / 256);
         if (blocks > sm_count()) blocks = sm_count();
         k_call_begin<<<blocks, 256, 0, st>>>(zf, zb, (double *)(ws + L.feats), (double *)(ws + L.bt),
-                                             n_apps, (uint32_t *)(ws + L.qcount), (int)(zero_bytes / 4));
+                                             n_apps);
         CS_TRY(cudaGetLastError());
     } else {
         CS_TRY(cudaMemcpyAsync(ws + L.feats, h_features, sizeof(double) * n * NF, cudaMemcpyHostToDevice, st));
         CS_TRY(cudaMemcpyAsync(ws + L.bt, h_base_time, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-        CS_TRY(cudaMemsetAsync(ws + L.qcount, 0, zero_bytes, st));
     }
 
     cs_grid dg = *h_grid;
@@ -1913,12 +2029,13 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     cs_solo_out so{(double *)(ws + L.solo_time), (int32_t *)(ws + L.solo_split),
                    (int32_t *)(ws + L.solo_clamps)};
     CS_RC(cs_prepare(net, (const double *)(ws + L.feats), (const double *)(ws + L.bt), n_apps, &dg,
-                     &t, so, stream));
+                     &t, so, (cs_counters *)(ws + L.qcount), (unsigned long long *)(ws + L.clamps),
+                     stream));
     cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
     CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
                               so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue),
-                              (uint32_t *)(ws + L.qcount), (unsigned long long *)(ws + L.clamps),
+                              (cs_counters *)(ws + L.qcount), (unsigned long long *)(ws + L.clamps),
                               h_weights ? (double *)(ws + L.W) : nullptr, CS_KERNEL_AUTO, stream));
     if (h_weights)
         CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
@@ -1940,7 +2057,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
                         (!h_solo.solo_split || e.h_solo_split) &&
                         (!h_solo.solo_clamps || e.h_solo_clamps) && (!h_clamps || e.h_clamps);
     if (zc_out) {
-        const int64_t items = 3 * (int64_t)LN + nb + 2;
+        const int64_t items = 3 * (int64_t)LN + nb + 4;
         int blocks = (int)((items + 255) / 256);
         if (blocks > sm_count()) blocks = sm_count();
         k_call_end<<<blocks, 256, 0, st>>>(e);
@@ -1950,7 +2067,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
         if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
         if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));
         if (h_clamps) CS_TRY(cudaMemcpyAsync(h_clamps, ws + L.clamps, 8 * (size_t)nb, cudaMemcpyDeviceToHost, st));
-        if (h_counters) CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
+        if (h_counters) CS_TRY(cudaMemcpyAsync(h_counters, ws + L.qcount, sizeof(cs_counters), cudaMemcpyDeviceToHost, st));
     }
 #undef CS_TRY
 #undef CS_RC

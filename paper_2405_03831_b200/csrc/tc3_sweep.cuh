@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             const uint32_t krow = tc::smem_u32(k12 + member * ROW32);   // + c * 2 * ROW32 * 4
 
             float best[L], second[L];
+            float mind = FLT_MAX;          // closest screened prediction to the 0.5 floor
             int idx[L], bcl[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; bcl[l] = 0; }
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                                    wo2[o], y2);
                 const float y = (y2.x + y2.y) + bo;
                 const int cl = y < 0.5f;
+                mind = fminf(mind, fabsf(y - 0.5f));
                 const float tm = fmaxf(y, 0.5f) * T_self;
                 const float tt = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
                 const uint32_t m = L == 1 ? 1u : masks[c];
@@ -433,6 +435,13 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 if (x >= 0 && x < n_cfg) epilogue(x, u % S);
             }
             }
+            // a prediction too close to the floor for the screen to count its
+            // clamp: k_resolve re-counts this row's clamps in fp64 instead
+            if (mind <= a.tau) {
+                if (live) push_row(a, pl, member);
+#pragma unroll
+                for (int l = 0; l < L; ++l) bcl[l] = 0;
+            }
 #pragma unroll
             for (int l = 0; l < L; ++l) clamps[l] += live ? bcl[l] : 0;
 
@@ -450,6 +459,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                         push_ambiguous(a, l, pl);
                     } else {
                         write_winner(a, l, pl, idx[l], co, best[l]);
+                        maybe_verify(a, l, pl, best[l], second[l]);
                         if (a.fused) clamps[l] += decide_write(a, l, pl, i, j, idx[l], co);
                     }
                 }

@@ -97,9 +97,17 @@ def n_pairs(n: int) -> int:
 
 @dataclass
 class SweepCounters:
-    queue_len: int
-    screen_error: float
-    clamps: np.ndarray
+    queue_len: int           # (pair, budget)s re-scanned exactly in fp64
+    screen_error: float      # largest screened-vs-fp64 relative gap (winners, near runner-ups)
+    clamps: np.ndarray       # per budget: floor clamps as the reference counts them
+    exact_rows: int = 0      # (pair, member) rows whose clamps were re-counted in fp64
+    verify_fail: int = 0     # sampled near-tie pairs whose exact re-scan disagreed
+
+    @property
+    def effective_error(self) -> float:
+        """The screen error the band must cover: the observed gap, or -- when a
+        sampled exact re-scan disagreed with the screen -- infinity."""
+        return float("inf") if self.verify_fail else self.screen_error
 
 
 def fp16_screen_safe(weights) -> bool:
@@ -184,8 +192,10 @@ class SweepPlan:
             self.solo_time = torch.empty((L, n), dtype=torch.float64, device=dev)
             self.solo_split = torch.empty((L, n), dtype=torch.int32, device=dev)
             self.solo_clamps = torch.empty((L, n), dtype=torch.int32, device=dev)
-            self.queue = torch.empty(L * P, dtype=torch.int64, device=dev)
-            self.counters = torch.zeros(2, dtype=torch.int32, device=dev)
+            # [0, L P): exact re-scan queue; [L P, (L + 2) P): rows whose floor
+            # clamps k_resolve re-counts in fp64
+            self.queue = torch.empty((L + 2) * P, dtype=torch.int64, device=dev)
+            self.counters = torch.zeros(nat.COUNTERS_BYTES // 4, dtype=torch.int32, device=dev)
             self.clamps = torch.zeros(L, dtype=torch.int64, device=dev)
             self.matrix = (torch.zeros((L, n, n), dtype=torch.float64, device=dev)
                            if with_matrix else None)
@@ -227,13 +237,13 @@ class SweepPlan:
         eps = self.rel_eps if rel_eps is None else float(rel_eps)
         cur = torch.cuda.current_stream(dev)
         st = cur.cuda_stream
-        self.counters.zero_()
-        self.clamps.zero_()
         tref = ctypes.byref(self.tables)
         cnt = _dptr(self.counters)
         if self.fused:
+            # k_tables also zeroes the counters and clamps for the screen
             nat.check(lib.cs_prepare(self.net.ref(), _dptr(d_features), _dptr(d_base_time), n,
-                                     self.dgrid.ref(), tref, self.solo_out, st), "cs_prepare")
+                                     self.dgrid.ref(), tref, self.solo_out, cnt,
+                                     _dptr(self.clamps), st), "cs_prepare")
             if self.P == 0:
                 return
             # the symmetric matrix is scattered in-kernel when this plan owns
@@ -255,6 +265,8 @@ class SweepPlan:
             if self.matrix is not None and w is None:
                 self.scatter(st)
             return
+        self.counters.zero_()
+        self.clamps.zero_()
         nat.check(lib.cs_build_tables(self.net.ref(), _dptr(d_features), n, self.dgrid.ref(),
                                       tref, st), "cs_build_tables")
         # solo splits run on a side stream, concurrently with the pair screen
@@ -275,7 +287,7 @@ class SweepPlan:
             sweep_events[1].record(cur)
         nat.check(lib.cs_resolve(self.net.ref(), tref, self.dgrid.ref(), _dptr(d_base_time),
                                  self.pair_begin, self.pair_end, self.pair_out, _dptr(self.queue),
-                                 cnt, st), "cs_resolve")
+                                 cnt, _dptr(self.clamps), st), "cs_resolve")
         cur.wait_stream(self._side)
         # decisions (+ the symmetric matrix when this plan owns the whole graph)
         w = _dptr(self.matrix) if (self.matrix is not None and self.P == n_pairs(n)) else None
@@ -297,7 +309,8 @@ class SweepPlan:
         c = self.counters.cpu().numpy()
         return SweepCounters(queue_len=int(c[0]),
                              screen_error=float(np.array([c[1]], dtype=np.int32).view(np.float32)[0]),
-                             clamps=self.clamps.cpu().numpy().astype(np.int64))
+                             clamps=self.clamps.cpu().numpy().astype(np.int64),
+                             exact_rows=int(np.uint32(c[2])), verify_fail=int(np.uint32(c[3])))
 
 
 def to_device_inputs(features, base_time, device) -> tuple:

@@ -82,8 +82,9 @@ class HostGraphCall:
             self.pairs = nat.CsPairOut()
         self._t_st, self.h_solo_time = _pinned((L, n), torch.float64)
         self._t_ss, self.h_solo_split = _pinned((L, n), torch.int32)
+        self._t_sc, self.h_solo_clamps = _pinned((L, n), torch.int32)
         self.solo = nat.CsSoloOut(nat.ptr(self.h_solo_time), nat.ptr(self.h_solo_split, nat.c_int32_p),
-                                  None)
+                                  nat.ptr(self.h_solo_clamps, nat.c_int32_p))
         # pinned like every other buffer: the call's graph reads / writes all
         # of them with zero-copy kernels or async copies
         self._t_cl, h_cl = _pinned((L,), torch.int64)
@@ -113,7 +114,7 @@ class HostGraphCall:
         network stay in the workspace after the first call)."""
         h2d = self.h_features.nbytes + self.h_base_time.nbytes
         d2h = self.h_weights.nbytes + self.h_solo_time.nbytes + self.h_solo_split.nbytes + \
-            self.h_clamps.nbytes
+            self.h_solo_clamps.nbytes + self.h_clamps.nbytes
         if self.with_records:
             d2h += self.h_idx.nbytes + self.h_ct.nbytes + self.h_ch.nbytes + self.h_pw.nbytes
         return h2d, d2h
@@ -130,7 +131,8 @@ class HostGraphCall:
         rc = self.lib.cs_build_graph_host(*self._args, stream)
         nat.check(rc, "cs_build_graph_host")
         out = {"weights": self.h_weights, "solo_time": self.h_solo_time,
-               "solo_split": self.h_solo_split, "clamps": self.h_clamps}
+               "solo_split": self.h_solo_split, "solo_clamps": self.h_solo_clamps,
+               "clamps": self.h_clamps}
         if self.with_records:
             out.update(corun_grid_index=self.h_idx, corun_time=self.h_ct,
                        corun_chosen=self.h_ch.astype(bool), weight=self.h_pw)

@@ -77,6 +77,7 @@ class SweepResult:
     clamps: np.ndarray               # (L,) floor clamps as the reference would count them
     queue_len: int                   # (pair, budget)s re-scanned exactly in fp64
     screen_error: float              # largest fp32-screen vs fp64 relative gap seen
+    exact_rows: int = 0              # rows whose floor clamps were re-counted in fp64
     matrix: Optional[np.ndarray] = field(default=None)   # (L, N, N) symmetric weights
 
     def corun_local_index(self, l: int) -> np.ndarray:
@@ -110,7 +111,7 @@ def run_plan(plan: SweepPlan, features: np.ndarray, base_time: np.ndarray,
             # a network far outside the trained range: the fp32 screen's observed
             # error is not well inside rel_eps -- widen the ambiguity band (more
             # pairs go to the exact fp64 resolve; results identical) and redo
-            while c.screen_error > 0.25 * eps and 16.0 * eps < 0.1:
+            while (c.screen_error > 0.25 * eps or c.verify_fail) and 16.0 * eps < 0.1:
                 eps = min(max(16.0 * eps, 16.0 * c.screen_error), 0.099)
                 plan.launch(d_f, d_b, rel_eps=eps)
                 c = plan.read_counters()
@@ -125,8 +126,9 @@ def run_plan(plan: SweepPlan, features: np.ndarray, base_time: np.ndarray,
                 solo_split=plan.solo_split.cpu().numpy(),
                 solo_clamps=plan.solo_clamps.cpu().numpy(),
                 clamps=c.clamps, queue_len=c.queue_len, screen_error=c.screen_error,
+                exact_rows=c.exact_rows,
                 matrix=plan.matrix.cpu().numpy() if (with_matrix and plan.matrix is not None) else None)
-    if res.screen_error > 0.25 * eps:
+    if res.screen_error > 0.25 * eps or c.verify_fail:
         raise RuntimeError(f"fp32 screen error {res.screen_error:.3g} is too close to rel_eps "
                            f"{eps:.3g}; argmin parity is no longer guaranteed")
     return res

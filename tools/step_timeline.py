@@ -24,7 +24,7 @@ def step():
     plan.counters.zero_(); plan.clamps.zero_()
     ev[0].record()
     nat.check(lib.cs_prepare(plan.net.ref(), _dptr(df), _dptr(db), n, plan.dgrid.ref(), tref,
-                             plan.solo_out, st), "prep")
+                             plan.solo_out, _dptr(plan.counters), _dptr(plan.clamps), st), "prep")
     ev[1].record()
     nat.check(lib.cs_pair_screen_fused(plan.net.ref(), tref, plan.dgrid.ref(), _dptr(db),
               _dptr(plan.solo_time), _dptr(plan.solo_clamps), 0, plan.P, plan.rel_eps,

@@ -5,7 +5,7 @@ import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np, torch
-from paper_2405_03831_b200 import core, fnn, synth
+from paper_2405_03831_b200 import _native as nat, core, fnn, synth
 from paper_2405_03831_b200.device import SweepPlan, to_device_inputs, _dptr
 from paper_2405_03831_b200.grid import KnobGrid
 
@@ -49,8 +49,8 @@ for n in [int(x) for x in (sys.argv[1:] or ["256", "1024"])]:
         lib, tref = plan.lib, ctypes.byref(plan.tables)
         st = lambda: torch.cuda.current_stream().cuda_stream
         prep = lambda: lib.cs_prepare(plan.net.ref(), _dptr(df), _dptr(db), n, plan.dgrid.ref(), tref,
-                                      plan.solo_out, st())
-        z = torch.zeros(2, dtype=torch.int32, device=plan.device)
+                                      plan.solo_out, _dptr(plan.counters), _dptr(plan.clamps), st())
+        z = torch.zeros(nat.COUNTERS_BYTES // 4, dtype=torch.int32, device=plan.device)
 
         def screen():
             z.zero_()

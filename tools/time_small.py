@@ -41,7 +41,7 @@ for n in (256, 4096):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps * 1e3
 
-    prep = lambda: lib.cs_prepare(plan.net.ref(), _dptr(df), _dptr(db), n, plan.dgrid.ref(), tref, plan.solo_out, st_of())
+    prep = lambda: lib.cs_prepare(plan.net.ref(), _dptr(df), _dptr(db), n, plan.dgrid.ref(), tref, plan.solo_out, _dptr(plan.counters), _dptr(plan.clamps), st_of())
     tabl = lambda: lib.cs_build_tables(plan.net.ref(), _dptr(df), n, plan.dgrid.ref(), tref, st_of())
     solo = lambda: lib.cs_solo(plan.net.ref(), tref, plan.dgrid.ref(), _dptr(db), plan.solo_out, st_of())
     res = lambda: lib.cs_resolve_fused(plan.net.ref(), tref, plan.dgrid.ref(), _dptr(db), _dptr(plan.solo_time), _dptr(plan.solo_clamps), 0, plan.P, plan.pair_out, _dptr(plan.queue), _dptr(plan.counters), _dptr(plan.clamps), None, st_of())
