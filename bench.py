@@ -534,7 +534,7 @@ def run_ours(args):
                          "api": "cs_build_graph_host (C ABI, pinned host buffers; D2H = N x N weights + "
                                 "solo times/splits + clamps)"}
         # second BASELINE metric: schedule time at this N (sweep + D2H + host matching)
-        jobs = synth.generate_workload(0, synth.mixed_archetypes(n1))
+        jobs = synth.generate_jobs(0, synth.mixed_archetypes(n1))
         from paper_2405_03831_b200 import core as _core
         inp = scheduler.SchedulerInput(tuple(jobs), sp1[-1], _core.SchedulingParams(window=n1),
                                        weights)

@@ -21,9 +21,9 @@ from .hwopt import PairDecision, decide_pair, optimize_corun, optimize_solo_pair
 from .matcher import PairGraph, brute_force_matching, matching_weight, min_weight_perfect_matching
 from .scheduler import (SchedulerInput, build_graph, predicted_makespan, schedule,
                         schedule_to_json, set_time)
-from .synth import generate_workload, mixed_archetypes
+from .simenv import (OracleParams, OracleSlowdownModel, SyntheticJobSpec, generate_workload,
+                     mixed_archetypes, oracle_slowdown)
 from .grid import KnobGrid
-from .analytic import OracleParams, OracleSlowdownModel, oracle_slowdown
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 

@@ -4,8 +4,8 @@ Reproduces ``simenv.generate_workload`` / ``mixed_archetypes``
 (simenv.py:264-311) bit-for-bit (pinned by tests/golden/workloads.json): one
 ``numpy.random.default_rng([seed, 100])`` stream, per job 18 uniform counter
 draws inside its archetype's ranges, then one base time in U(15, 45) s.
-Only the generator lives here; the analytic oracle, dataset labelling and
-policy harness of simenv are out of scope.
+``simenv.generate_workload`` wraps the same draws in ``SyntheticJobSpec``s,
+exactly as the reference returns them.
 """
 
 from __future__ import annotations
@@ -58,7 +58,8 @@ def job_ids(archetypes: Sequence[str]) -> list:
     return [f"job{k:02d}-{a}" for k, a in enumerate(archetypes)]
 
 
-def generate_workload(seed: int, archetypes: Sequence[str]) -> list:
-    """JobProfiles in the reference's order and naming (``jobNN-<archetype>``)."""
+def generate_jobs(seed: int, archetypes: Sequence[str]) -> list:
+    """The JobProfiles of ``simenv.generate_workload`` (``[s.job for s in ...]``),
+    in the reference's order and naming (``jobNN-<archetype>``)."""
     feats, bt = workload_arrays(seed, archetypes)
     return [JobProfile(jid, feats[k], bt[k]) for k, jid in enumerate(job_ids(archetypes))]

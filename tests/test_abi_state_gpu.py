@@ -128,7 +128,7 @@ def test_retained_workspace_follows_network_changes(weights):
 
 
 def test_concurrent_decide_pair_equals_serial(weights):
-    jobs = synth.generate_workload(7, synth.mixed_archetypes(40))
+    jobs = synth.generate_jobs(7, synth.mixed_archetypes(40))
     space = core.default_space(400.0)
     pairs = [(i, j) for i in range(0, 40, 3) for j in range(i + 1, 40, 5)]
     serial = [cs.decide_pair(weights, jobs[i], jobs[j], space) for i, j in pairs]

@@ -23,7 +23,7 @@ def _model(doc_entry):
 
 
 def _jobs(n, seed):
-    return synth.generate_workload(seed, synth.mixed_archetypes(n))
+    return synth.generate_jobs(seed, synth.mixed_archetypes(n))
 
 
 def test_scalar_restatement_matches_reference_decisions():

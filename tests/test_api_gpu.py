@@ -17,7 +17,7 @@ def _hc(t):
 
 def test_decide_pair_matches_reference_samples(weights, samples):
     entry = samples["n4096_400"]
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(4096))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(4096))
     space = space_for(entry)
     configs = core.enumerate_corun_configs(space)
     splits = core.enumerate_solo_splits(space)
@@ -38,7 +38,7 @@ def test_decide_pair_matches_reference_samples(weights, samples):
 @pytest.mark.parametrize("budget", ["400", "350"])
 def test_build_graph_and_schedule_match_reference(weights, paper20, budget):
     sp = paper20["spaces"][budget]
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(20))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(20))
     space = core.default_space(float(budget))
     inp = cs.SchedulerInput(tuple(jobs), space, core.SchedulingParams(window=20), weights)
     estimator.clamp_stats.reset()
@@ -76,7 +76,7 @@ def _assert_matching_parity(graph, ours, ref_pairs, ref_weight):
 
 
 def test_full_256_schedule_matches_reference_matching(weights, n256):
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(256))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(256))
     inp = cs.SchedulerInput(tuple(jobs), core.default_space(400.0),
                             core.SchedulingParams(window=256), weights)
     graph = cs.build_graph(inp)
@@ -86,7 +86,7 @@ def test_full_256_schedule_matches_reference_matching(weights, n256):
 
 
 def test_empty_search_spaces_raise_like_the_reference(weights):
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(2))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(2))
     with pytest.raises(core.ValidationError, match="no co-run configs"):
         cs.optimize_corun(weights, jobs[0], jobs[1], core.default_space(300.0))
     # 300 W has solo splits but no co-run level: the solo optimizer still works
@@ -99,7 +99,7 @@ def test_empty_search_spaces_raise_like_the_reference(weights):
 
 
 def test_scalar_predictions_match_sweep(weights):
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(6))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(6))
     space = core.default_space(400.0)
     d = cs.decide_pair(weights, jobs[2], jobs[5], space)
     t = cs.corun_time(weights, core.JobSet((jobs[2], jobs[5])), d.corun_config, space)
@@ -111,7 +111,7 @@ def test_scalar_predictions_match_sweep(weights):
 def test_graph_csv_fast_path_matches_generic(tmp_path, weights):
     """graph_to_csv on a sweep graph (flag arrays, no PairDecision objects) writes
     exactly what the generic per-edge path writes (matcher.py:132-142)."""
-    jobs = synth.generate_workload(2, synth.mixed_archetypes(40))
+    jobs = synth.generate_jobs(2, synth.mixed_archetypes(40))
     inp = cs.SchedulerInput(tuple(jobs), core.default_space(400.0),
                             core.SchedulingParams(window=40), weights)
     g = cs.build_graph(inp)

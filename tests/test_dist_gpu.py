@@ -61,7 +61,7 @@ def test_sharded_sweep_rebuilds_the_graph(tmp_path, weights, world):
                        start_method="spawn", join=True)
     got = dict(np.load(out))
     spaces = [core.default_space(400.0), core.default_space(350.0)]
-    single = sweep_pairs(weights, synth.generate_workload(0, synth.mixed_archetypes(n)), spaces)
+    single = sweep_pairs(weights, synth.generate_jobs(0, synth.mixed_archetypes(n)), spaces)
     assert np.array_equal(got["matrix"], single.matrix)
     F, T = workload(n)
     ref = oracle.sweep(weights, F, T, KnobGrid(spaces))

@@ -45,7 +45,7 @@ def test_binding_loads_and_binds_symbols():
 @pytest.mark.parametrize("n,budget", [(20, 400.0), (64, 350.0)])
 def test_binding_build_graph_matches_oracle_and_dropin(weights, n, budget):
     b = _binding()
-    jobs = synth.generate_workload(1, synth.mixed_archetypes(n))
+    jobs = synth.generate_jobs(1, synth.mixed_archetypes(n))
     space = core.default_space(budget)
     inp = cs.SchedulerInput(tuple(jobs), space, core.SchedulingParams(window=n), weights)
     estimator.clamp_stats.reset()

@@ -30,7 +30,7 @@ class Analytic:
 
 
 def _jobs(n):
-    return cs.generate_workload(0, cs.mixed_archetypes(n))
+    return [s.job for s in cs.generate_workload(0, cs.mixed_archetypes(n))]
 
 
 def test_ties_take_first_config_and_corun():

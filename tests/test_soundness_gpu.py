@@ -29,7 +29,7 @@ def _net(w, w1=None, b1=None, wo=None, bo=None):
 
 
 def _check_exact(net, n, seed, spaces, kernel="tcgen05"):
-    jobs = synth.generate_workload(seed, synth.mixed_archetypes(n))
+    jobs = synth.generate_jobs(seed, synth.mixed_archetypes(n))
     res = sweep_pairs(net, jobs, spaces, with_matrix=False, kernel=kernel)
     F, T = workload(n, seed)
     grid = KnobGrid(spaces)

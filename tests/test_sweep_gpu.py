@@ -23,7 +23,7 @@ REL = 1e-12
 
 
 def _jobs(n, seed=0):
-    return synth.generate_workload(seed, synth.mixed_archetypes(n))
+    return synth.generate_jobs(seed, synth.mixed_archetypes(n))
 
 
 def _assert_same_as_oracle(res, ref, l=0):
@@ -65,6 +65,31 @@ def test_full_reference_graph_256(weights, n256):
     assert np.max(np.abs(res.weight[0] - n256["winning_time"]) / n256["winning_time"]) <= REL
     F, T = workload(256)
     _assert_same_as_oracle(res, oracle.sweep(weights, F, T, KnobGrid([core.default_space(400.0)])))
+
+
+def _assert_clamps_exact(res, ref, n):
+    """clamp_stats over build_graph (estimator.py:98-109): every co-run
+    prediction of every pair plus both members' solo splits once per pair."""
+    for l in range(res.clamps.shape[0]):
+        solo_part = (n - 1) * int(res.solo_clamps[l].sum())
+        assert int(res.clamps[l]) == int(ref["corun_clamps"][l]) + solo_part, l
+
+
+def test_all_pairs_1024_five_budgets_bit_exact(weights):
+    """BASELINE config 3 in full: all 523,776 pairs x the 220-config union grid
+    for the five budgets 300..400 W; every budget's argmin, flag, CoRunTime,
+    weight and clamp count equal the fp64 oracle."""
+    n = 1024
+    spaces = [core.ConfigSpace(p_total=p, cap_sum_levels=(300, 325, 350, 375, 400))
+              for p in (300.0, 325.0, 350.0, 375.0, 400.0)]
+    grid = KnobGrid(spaces)
+    F, T = workload(n)
+    res = sweep_pairs(weights, _jobs(n), spaces, with_matrix=False)
+    ref = oracle.sweep(weights, F, T, grid)
+    for l in range(5):
+        _assert_same_as_oracle(res, ref, l)
+    _assert_clamps_exact(res, ref, n)
+    assert res.screen_error < 2.5e-6
 
 
 def test_five_budget_sweep_1024_shards(weights):
@@ -192,10 +217,11 @@ def test_cuda_is_the_path():
 
 @pytest.mark.parametrize("grid_kind", ["default400", "fine400"])
 def test_all_pairs_4096_bit_exact_against_oracle(weights, grid_kind):
-    """Every one of the 8.4M pairs at N=4,096: argmin index, flag, CoRunTime and
-    weight bit-identical to the fp64 oracle (threaded C restatement, ~30 s of
-    host CPU on the GPU box), so the screen threshold (rel_eps = 1e-5) never
-    changes a result at full size."""
+    """Every one of the 8.4M pairs at N=4,096, on the default grid (100 configs)
+    and on the fine 6.25 W grid (340 configs, BASELINE config 5): argmin index,
+    flag, CoRunTime, weight and clamp count bit-identical to the fp64 oracle
+    (threaded C restatement, ~15 s / ~50 s of host CPU on the GPU box), so the
+    screen threshold (rel_eps = 1e-5) never changes a result at full size."""
     n = 4096
     if grid_kind == "default400":
         spaces = [core.default_space(400.0)]
@@ -205,16 +231,12 @@ def test_all_pairs_4096_bit_exact_against_oracle(weights, grid_kind):
                                    p_total=400.0)]
     res = sweep_pairs(weights, _jobs(n), spaces, with_matrix=False)
     F, T = workload(n)
-    P = n * (n - 1) // 2
-    # the fine grid costs 3.4x the default: check a third of its pairs (3 spread ranges)
-    ranges = [(0, P)] if grid_kind == "default400" else \
-        [(0, P // 9), (P // 2 - P // 18, P // 2 + P // 18), (P - P // 9, P)]
-    for b, e in ranges:
-        ref = oracle.sweep(weights, F, T, res.grid, b, e)
-        assert np.array_equal(res.corun_grid_index[0, b:e], ref["corun_grid_index"][0])
-        assert np.array_equal(res.corun_chosen[0, b:e], ref["corun_chosen"][0])
-        assert np.array_equal(res.corun_time[0, b:e], ref["corun_time"][0])
-        assert np.array_equal(res.weight[0, b:e], ref["weight"][0])
+    ref = oracle.sweep(weights, F, T, res.grid)
+    assert np.array_equal(res.corun_grid_index[0], ref["corun_grid_index"][0])
+    assert np.array_equal(res.corun_chosen[0], ref["corun_chosen"][0])
+    assert np.array_equal(res.corun_time[0], ref["corun_time"][0])
+    assert np.array_equal(res.weight[0], ref["weight"][0])
+    _assert_clamps_exact(res, ref, n)
     assert res.screen_error < 2.5e-6
 
 

@@ -26,7 +26,7 @@ def _check(res, ref, L):
     (256, 0, (400.0,))])
 def test_screen_kernels_match_oracle(weights, kernel, n, seed, budgets):
     spaces = [core.default_space(p) for p in budgets]
-    jobs = synth.generate_workload(seed, synth.mixed_archetypes(n))
+    jobs = synth.generate_jobs(seed, synth.mixed_archetypes(n))
     res = sweep_pairs(weights, jobs, spaces, with_matrix=False, kernel=kernel)
     F, T = workload(n, seed)
     ref = oracle.sweep(weights, F, T, KnobGrid(spaces))
@@ -39,7 +39,7 @@ def test_five_budgets_and_fine_grid_shards(weights, kernel):
     levels = (300, 325, 350, 375, 400)
     spaces = [core.ConfigSpace(p_total=p, cap_sum_levels=levels) for p in (300.0, 325.0, 350.0, 375.0, 400.0)]
     n = 1024
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(n))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(n))
     F, T = workload(n)
     b, e = 123_456, 123_456 + 5000
     res = sweep_pairs(weights, jobs, spaces, b, e, with_matrix=False, kernel=kernel)
@@ -60,7 +60,7 @@ def test_out_of_fp16_range_network_falls_back_and_stays_exact(weights):
                              weights.w_out, weights.b_out, weights.feature_bounds)
     assert fp16_screen_safe(weights) and not fp16_screen_safe(big)
     n = 48
-    jobs = synth.generate_workload(5, synth.mixed_archetypes(n))
+    jobs = synth.generate_jobs(5, synth.mixed_archetypes(n))
     spaces = [core.default_space(400.0)]
     res = sweep_pairs(big, jobs, spaces, with_matrix=False)
     F, T = workload(n, 5)

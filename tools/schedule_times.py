@@ -10,7 +10,7 @@ from paper_2405_03831_b200 import core, fnn, matcher, scheduler, synth
 w = fnn.load_weights(os.path.join(ROOT, "tests", "golden", "weights.json"))
 out = {}
 for n in [int(x) for x in (sys.argv[1:] or ["20", "256", "1024", "4096"])]:
-    jobs = synth.generate_workload(0, synth.mixed_archetypes(n))
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(n))
     inp = scheduler.SchedulerInput(tuple(jobs), core.default_space(400.0),
                                    core.SchedulingParams(window=n), w)
     scheduler.build_graph(inp)                       # warm the plan cache / GPU
