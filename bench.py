@@ -6,23 +6,36 @@ A step is one full build_graph sweep of the workload with inputs resident in
 HBM: per-app/per-knob tables -> solo splits -> fused pair x knob sweep ->
 exact re-scan of near-ties -> symmetric N x N weight scatter, replayed as one
 CUDA graph.  L2 is flushed (256 MiB memset) before every step, outside the
-events.  `value` = reference-equivalent (pair, config) evaluations (P x sum of
-per-budget configs) / sum of the per-step CUDA-event times, max over ranks.
+events.  `value` = unique (pair, config) evaluations per second: P x the
+configs of the union grid of the swept budgets (for one budget, exactly the
+reference's P x C); `value_reference_equivalent` counts P x the sum of the
+per-budget config counts, the evaluations the reference makes (they differ
+only for the 5-budget sweep: 220 unique vs 610 per pair).
 
 `e2e` = the same metric through the host-buffer C ABI (cs_build_graph_host):
-pinned host features in, H2D, the five kernels, D2H of the N x N weights and
-the per-pair records, all inside the timed region (wall clock; the call
-synchronizes).  `roofline` = the dominant kernel (k_sweep), its algorithmic
-flops (1,368 per unit: layer 2 + head for both members after the exact layer-1
+pinned host features in, the kernels, D2H of the N x N weights, the solo
+splits and the per-pair decision records (config index, CoRunTime, co-run
+flag), all inside the timed region (wall clock; the call synchronizes).
+`roofline` = the dominant kernel (k_sweep_tc3), its algorithmic flops (1,368
+per unique unit: layer 2 + head for both members after the exact layer-1
 factorization) over its own event-timed duration against the
-measured dense bf16 tensor peak.  `cpu_baseline` / `--impl reference` = the
-oracle port (oracle/cosched_oracle.c, factored fp64, all host threads) on a
-bounded sample of the same workload.
+measured dense bf16 tensor peak; `roofline_issue` = the same kernel against
+the CUDA-core issue rate, the bound that actually binds it.
+`cpu_baseline` / `--impl reference` = the oracle port (oracle/cosched_oracle.c,
+factored fp64, all host threads) on a bounded sample of the same workload;
+`cpu_baseline_reference` = the UNMODIFIED reference (baseline/_ref, staged by
+tools/stage_reference.sh) timed on the same host: a process pool over
+hwopt.decide_pair on a seeded pair sample, and build_graph(jobs=cores) at
+paper scale.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): weak scaling -- the app count
-grows with sqrt(N) so every GPU sweeps the same number of pairs; each rank
-sweeps its contiguous pair shard, then one NCCL all-gather of the records and
-a device scatter build the full matrix on every rank.
+With --gpus 1 and the default workload the line also carries `workloads`:
+the same measurements for BASELINE's 4,096-app and 1,024-app x 5-budget
+configs.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): STRONG scaling of the 4,096-app
+config (BASELINE.json config 4) unless --workload is given: rank r sweeps its
+contiguous pair shard, ONE NCCL gather moves the 11-byte records to rank 0,
+which rebuilds the full record set and matrix on its device.
 """
 
 from __future__ import annotations
@@ -210,21 +223,28 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-def cpu_baseline(weights, name, seconds=12.0, threads=None, n_override=None):
+def bench_config(name, n, grid, world):
+    """The workload-identifying `config` -- identical on both arms."""
+    P = n * (n - 1) // 2
+    return {"workload": WORKLOADS[name][3], "name": name, "n_apps": n, "pairs": P,
+            "configs_per_pair": grid.n_grid, "reference_configs_per_pair": grid.units_per_pair(),
+            "budgets_w": [s.p_total for s in grid.spaces],
+            "parallelism": f"pair shards x{world}" if world > 1 else "1 GPU"}
+
+
+def cpu_baseline(weights, name, seconds=12.0, threads=None):
     """Oracle port (factored fp64, threaded) on a bounded sample of the workload."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle  # checker / baseline only
     from paper_2405_03831_b200 import synth
     from paper_2405_03831_b200.grid import KnobGrid
     n, spaces = spaces_for(name)
-    if n_override:
-        n = n_override
     grid = KnobGrid(spaces)
     F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
     P = n * (n - 1) // 2
     threads = threads or os.cpu_count() or 1
     # sample: a contiguous pair range sized to ~1 s per pass, repeated for `seconds`
-    chunk = min(P, max(threads * 64, int(2.0e6 / max(1, grid.units_per_pair()) * threads / 8)))
+    chunk = min(P, max(threads * 64, int(2.0e6 / max(1, grid.n_grid) * threads / 8)))
     oracle.sweep(weights, F, T, grid, 0, min(chunk, P), threads)  # warm
     done, t0, passes = 0, time.perf_counter(), 0
     while True:
@@ -235,11 +255,95 @@ def cpu_baseline(weights, name, seconds=12.0, threads=None, n_override=None):
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
-    units = done * grid.units_per_pair()
+    units = done * grid.n_grid
     return {"value": units / dt, "unit": "configs/s", "cores": threads, "kind": "port",
             "sample": f"{passes} passes x {chunk} pairs of the {n}-app workload "
-                      f"({grid.units_per_pair()} configs/pair) = {units:.3g} configs in {dt:.1f}s; "
+                      f"({grid.n_grid} unique configs/pair) = {units:.3g} configs in {dt:.1f}s; "
                       f"oracle/cosched_oracle.c factored fp64, {threads} threads"}
+
+
+_REF_SCRIPT = r"""
+import json, multiprocessing as mp, os, sys, time
+import numpy as np
+from cosched import core, fnn, hwopt, scheduler, simenv
+assert 'baseline' in os.path.abspath(core.__file__), core.__file__
+cfg = json.loads(sys.argv[1])
+W = fnn.load_weights(cfg["weights"])
+n = cfg["n"]
+jobs = [s.job for s in simenv.generate_workload(0, simenv.mixed_archetypes(n))]
+spaces = [core.ConfigSpace(**kw) for kw in cfg["spaces"]]
+if cfg.get("caps"):
+    core.CPU_CAPS, core.GPU_CAPS = tuple(cfg["caps"][0]), tuple(cfg["caps"][1])
+P = n * (n - 1) // 2
+rng = np.random.default_rng(1234)
+k = min(P, cfg["pairs"])
+pick = np.sort(rng.choice(P, size=k, replace=False))
+iu, ju = np.triu_indices(n, 1)
+work = [(int(iu[p]), int(ju[p])) for p in pick]
+
+def one(ij):
+    return [hwopt.decide_pair(W, jobs[ij[0]], jobs[ij[1]], sp).corun_chosen for sp in spaces]
+
+procs = os.cpu_count() or 1
+with mp.get_context("fork").Pool(procs) as pool:
+    pool.map(one, work[:procs])                    # warm the workers
+    t0 = time.perf_counter()
+    pool.map(one, work, chunksize=max(1, len(work) // (4 * procs)))
+    dt = time.perf_counter() - t0
+configs = sum(len(core.enumerate_corun_configs(sp)) for sp in spaces)
+out = {"decide_pair_pool": {"value": k * configs / dt, "unit": "configs/s", "processes": procs,
+                            "pairs": k, "seconds": dt,
+                            "sample": f"{k} seeded pairs (default_rng(1234)) of the {n}-app workload"
+                                      f" x {configs} reference configs/pair, unmodified "
+                                      f"hwopt.decide_pair in a {procs}-process pool"}}
+if cfg.get("build_graph_n"):
+    m = cfg["build_graph_n"]
+    jb = [s.job for s in simenv.generate_workload(0, simenv.mixed_archetypes(m))]
+    inp = scheduler.SchedulerInput(tuple(jb), spaces[-1], core.SchedulingParams(window=m), W)
+    t0 = time.perf_counter()
+    scheduler.build_graph(inp, jobs=procs)
+    dt = time.perf_counter() - t0
+    c = len(core.enumerate_corun_configs(spaces[-1]))
+    out["build_graph_threads"] = {"value": m * (m - 1) // 2 * c / dt, "unit": "configs/s",
+                                  "threads": procs, "n_apps": m, "seconds": dt,
+                                  "api": "scheduler.build_graph(inp, jobs=os.cpu_count())"}
+print(json.dumps(out))
+"""
+
+
+def cpu_baseline_reference(name, pairs=2000, build_graph_n=20, timeout=240):
+    """The unmodified reference (baseline/_ref) on this host, in a subprocess:
+    a process pool over hwopt.decide_pair on a seeded pair sample of the
+    workload, and build_graph(jobs=cores) at paper scale.  None if absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "cosched")):
+        return None
+    n, spaces = spaces_for(name)
+    caps = None
+    if WORKLOADS[name][2] == "fine":
+        caps = [list(FINE_CPU), list(FINE_GPU)]
+    cfg = {"weights": os.path.join(ROOT, "tests", "golden", "weights.json"), "n": n,
+           "pairs": pairs, "build_graph_n": build_graph_n, "caps": caps,
+           "spaces": [{"p_total": s.p_total, "cap_sum_levels": list(s.cap_sum_levels),
+                       "cpu_caps": list(s.cpu_caps), "gpu_caps": list(s.gpu_caps)} for s in spaces]}
+    env = dict(os.environ, PYTHONPATH=ref, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1")
+    try:
+        res = subprocess.run([sys.executable, "-c", _REF_SCRIPT, json.dumps(cfg)], env=env,
+                             capture_output=True, text=True, timeout=timeout, cwd=ref)
+    except subprocess.TimeoutExpired:
+        return {"error": f"timed out after {timeout}s"}
+    if res.returncode != 0:
+        return {"error": res.stderr.strip().splitlines()[-1] if res.stderr else "failed"}
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), None)
+    except OSError:
+        model = None
+    out["cpu_model"] = model
+    out["cores"] = os.cpu_count()
+    out["kind"] = "reference"
+    return out
 
 
 def run_reference(args):
@@ -248,6 +352,7 @@ def run_reference(args):
     Each of the W + K steps is one bounded pass over a contiguous pair range of
     the workload, sized from a calibration pass so the whole run takes ~90 s."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -255,9 +360,10 @@ def run_reference(args):
     from paper_2405_03831_b200 import synth
     from paper_2405_03831_b200.grid import KnobGrid
     weights = load_weights()
-    n, spaces = spaces_for(args.workload)
+    name = workload_name(args, world)
+    n, spaces = spaces_for(name)
     grid = KnobGrid(spaces)
-    upp = grid.units_per_pair()
+    upp = grid.n_grid
     P = n * (n - 1) // 2
     F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
     threads = os.cpu_count() or 1
@@ -278,13 +384,13 @@ def run_reference(args):
             vals.append(chunk * upp / dt)
     value = float(np.mean(vals))
     sample = (f"{args.steps} timed passes x {chunk} contiguous pairs of the {n}-app workload "
-              f"({upp} configs/pair); oracle/cosched_oracle.c factored fp64 port, {threads} threads")
+              f"({upp} unique configs/pair); oracle/cosched_oracle.c factored fp64 port, "
+              f"{threads} threads")
     line = {"impl": "reference", "metric": "(pair,knob) configs evaluated/sec", "value": value,
             "unit": "configs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": chunk * upp / value * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.workload][3], "n_apps": n, "pairs": P,
-                       "configs_per_pair": upp, "sample_pairs_per_step": chunk},
+            "ms_per_step": chunk * upp / value * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": bench_config(name, n, grid, world),
             "cpu_baseline": {"value": value, "unit": "configs/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0,
@@ -292,12 +398,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def issue_roofline(args, kernel_ms, world):
+def issue_roofline(name, kernel, kernel_ms, world):
     """The binding roofline of the sweep kernel: CUDA-core instruction issue
     (148 SMs x 4 schedulers x 1 warp-instruction/clock at the max SM clock).
     Instructions per launch come from the committed ncu capture of the same
     workload (1-GPU launch), so this is reported for world == 1 only."""
-    inst = measured_issue(args.workload, args.kernel)
+    inst = measured_issue(name, kernel)
     if not inst or world != 1:
         return None
     import torch
@@ -314,13 +420,158 @@ def issue_roofline(args, kernel_ms, world):
             "source": "smsp__inst_executed.sum of the ncu capture (profiles/issue.json)"}
 
 
+def roofline(name, kernel, kernel_ms, units, step_ms):
+    tf, _, src = measured_peaks()
+    achieved = FLOPS_PER_UNIT * units / (kernel_ms / 1e3) / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": tf, "unit": "TFLOP/s",
+            "frac": achieved / tf, "traffic": measured_traffic(name, kernel),
+            "kernel": {"tcgen05": "k_sweep_tc3<L,4,2,3> (tcgen05, A in TMEM)",
+                       "simt": "k_sweep (SIMT fp32)"}[kernel],
+            "kernel_ms": kernel_ms, "flops_per_unit": FLOPS_PER_UNIT,
+            "units_per_launch": units, "unit_def": "unique (pair, config)",
+            "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
+            "kernel_share_of_step": kernel_ms / step_ms}
+
+
+def workload_name(args, world):
+    if args.workload:
+        return args.workload
+    return "n4096" if world > 1 else "n256"
+
+
 # --------------------------------------------------------------------------
-def run_ours(args):
+def measure_single(args, name, steps, warmup, dev, weights, event_every, e2e=True,
+                   schedule=True):
+    """One workload on one GPU: the timed CUDA-graph steps, the kernel events,
+    the e2e host-ABI call and (optionally) the schedule time."""
     import torch
-    import torch.distributed as dist
     from paper_2405_03831_b200 import synth
     from paper_2405_03831_b200.device import SweepPlan, to_device_inputs
     from paper_2405_03831_b200.grid import KnobGrid
+
+    n, spaces = spaces_for(name)
+    grid = KnobGrid(spaces)
+    P = n * (n - 1) // 2
+    units = P * grid.n_grid
+    units_ref = P * grid.units_per_pair()
+    F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
+    d_f, d_b = to_device_inputs(F, T, dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev_s = torch.cuda.Event(enable_timing=True, external=True)
+    ev_e = torch.cuda.Event(enable_timing=True, external=True)
+    plan = SweepPlan(weights, grid, n, device=dev, with_matrix=True, kernel=args.kernel)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            plan.launch(d_f, d_b)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize(dev)
+    # two captures of the same step: with the kernel events (every
+    # event_every'th timed step: the dominant kernel's own duration) and
+    # without (an event between two kernels costs the graph its launch overlap)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        plan.launch(d_f, d_b, (ev_s, ev_e))
+    graph_plain = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_plain):
+        plan.launch(d_f, d_b)
+    for _ in range(warmup):
+        flush.zero_()
+        graph.replay()
+    torch.cuda.synchronize(dev)
+    c = plan.read_counters()
+
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms, sweep_ms = [], []
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index or 0) as clk:
+        t_wall = time.perf_counter()
+        for k in range(steps):
+            flush.zero_()                       # L2 flush, outside the step events
+            sample = k % event_every == 0
+            st.record()
+            (graph if sample else graph_plain).replay()
+            en.record()
+            en.synchronize()
+            step_ms.append(st.elapsed_time(en))
+            if sample:
+                sweep_ms.append(ev_s.elapsed_time(ev_e))
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t_wall
+    total_ms = float(sum(step_ms))
+    sweep_avg = float(np.mean(sweep_ms))
+    ms = total_ms / steps
+    out = {"value": units * steps / (total_ms / 1e3),
+           "value_reference_equivalent": units_ref * steps / (total_ms / 1e3),
+           "unit": "configs/s", "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "config": bench_config(name, n, grid, 1),
+           "roofline": roofline(name, args.kernel, sweep_avg, units, ms),
+           "roofline_issue": issue_roofline(name, args.kernel, sweep_avg, 1),
+           "gpu_launches": plan.launches_per_run * steps,
+           "clocks": clk.summary(),
+           "screen": {"queue_len": c.queue_len, "max_rel_gap": c.screen_error,
+                      "verify_fail": c.verify_fail, "exact_clamp_rows": c.exact_rows},
+           "wall_s_timed_region": wall}
+    del graph, graph_plain, plan, flush
+    if e2e:
+        from paper_2405_03831_b200.host_abi import HostGraphCall
+        # the call returns what a Schedule needs: the N x N weights, the solo
+        # splits and every pair's decision record (config index, CoRunTime, flag)
+        call = HostGraphCall(weights, grid, n, device=dev, with_records=True, pair_weight=False)
+        call.h_features[...] = F
+        call.h_base_time[...] = T
+        for _ in range(max(2, min(warmup, 5))):
+            call()
+        k = max(3, min(steps, 200 if n <= 512 else 10))
+        ts = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            call()
+            ts.append(time.perf_counter() - t0)
+        h2d, d2h = call.bytes_per_call()
+        call.close()
+        out["e2e"] = {"value": units / float(np.mean(ts)), "unit": "configs/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": k,
+                      "ms_per_call": float(np.mean(ts)) * 1e3,
+                      "api": "cs_build_graph_host (C ABI, pinned host buffers; D2H = N x N weights "
+                             "+ per-pair index/CoRunTime/flag + solo times/splits/clamps)"}
+        del call
+    if schedule:
+        out["schedule_e2e_s"] = schedule_time(n, spaces, weights)
+    torch.cuda.empty_cache()
+    return out
+
+
+def schedule_time(n, spaces, weights):
+    """BASELINE's second metric: profiles + weights -> Schedule (sweep, D2H,
+    native matching, emission), wall clock."""
+    from paper_2405_03831_b200 import core as _core, matcher, scheduler, synth
+    jobs = synth.generate_jobs(0, synth.mixed_archetypes(n))
+    inp = scheduler.SchedulerInput(tuple(jobs), spaces[-1], _core.SchedulingParams(window=n), weights)
+    # HardwareConfig validates caps against the module constants (core.py:121-128
+    # in the reference): a non-default cap grid needs them patched, exactly as
+    # the reference's own oracle run does
+    saved = (_core.CPU_CAPS, _core.GPU_CAPS)
+    _core.CPU_CAPS, _core.GPU_CAPS = spaces[-1].cpu_caps, spaces[-1].gpu_caps
+    try:
+        scheduler.build_graph(inp)            # warm (plan cache, GPU path)
+        t0 = time.perf_counter()
+        graph = scheduler.build_graph(inp)
+        t1 = time.perf_counter()
+        matched = matcher.min_weight_perfect_matching(graph)
+        t2 = time.perf_counter()
+        scheduler.emit_schedule(inp, graph, matched)
+        t3 = time.perf_counter()
+    finally:
+        _core.CPU_CAPS, _core.GPU_CAPS = saved
+    return {"total": t3 - t0, "build_graph": t1 - t0, "matching": t2 - t1, "emit": t3 - t2,
+            "n_apps": n}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -333,166 +584,150 @@ def run_ours(args):
         raise SystemExit(f"{world} ranks but {ndev} GPU(s)")
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
-    if world > 1:
-        backend = os.environ.get("COSCHED_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
-
     weights = load_weights()
-    n, spaces = spaces_for(args.workload)
-    if world > 1:   # weak scaling: pairs per GPU held at the 1-GPU count
-        n = int(round(n * math.sqrt(world) / 2.0)) * 2
+    name = workload_name(args, world)
+
+    if world == 1:
+        res = measure_single(args, name, args.steps, args.warmup, dev, weights, args.event_every,
+                             e2e=not args.no_e2e, schedule=not args.no_e2e)
+        line = {"metric": "(pair,knob) configs evaluated/sec", "value": res["value"],
+                "unit": "configs/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "fp32 screen / fp64 exact re-evaluation",
+                "data": "synthetic: simenv-equivalent workload (seed 0) + acceptance-recipe "
+                        "trained weights"}
+        line.update({k: v for k, v in res.items() if k not in ("steps", "warmup", "ms_per_step",
+                                                                "unit", "value")})
+        line["method"] = {"l2": "flushed before every step (256 MiB memset, outside the events)",
+                          "kernel_events": f"sweep kernel timed on every {args.event_every}th step "
+                                           "(same graph + 2 events)",
+                          "step": "CUDA graph: k_tables (+solo splits, counters) -> k_sweep_tc3 "
+                                  "(+decide, scatter) -> k_resolve (+decide, clamp re-counts)"}
+        if not args.no_subresults and args.workload is None:
+            subs = {}
+            for sub in ("n4096", "n1024x5"):
+                subs[sub] = measure_single(args, sub, 10, 3, dev, weights, 1,
+                                           e2e=not args.no_e2e, schedule=not args.no_e2e)
+            line["workloads"] = subs
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(weights, name, seconds=args.cpu_seconds)
+            ref = cpu_baseline_reference(name)
+            if ref is not None:
+                line["cpu_baseline_reference"] = ref
+        print(json.dumps(line), flush=True)
+        return
+    run_multi(args, name, world, rank, local_rank, dev, weights)
+
+
+def run_multi(args, name, world, rank, local_rank, dev, weights):
+    """N ranks, one per GPU: strong scaling of one workload over pair shards."""
+    import torch
+    import torch.distributed as dist
+    from paper_2405_03831_b200 import synth
+    from paper_2405_03831_b200.device import to_device_inputs
+    from paper_2405_03831_b200.dist import ShardedSweep
+    from paper_2405_03831_b200.grid import KnobGrid
+
+    backend = os.environ.get("COSCHED_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    n, spaces = spaces_for(name)
     grid = KnobGrid(spaces)
     P = n * (n - 1) // 2
-    upp = grid.units_per_pair()
     F, T = synth.workload_arrays(0, synth.mixed_archetypes(n))
     d_f, d_b = to_device_inputs(F, T, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    graph_mode = "cuda-graph"
     ev_s = torch.cuda.Event(enable_timing=True, external=True)
     ev_e = torch.cuda.Event(enable_timing=True, external=True)
-    if world == 1:
-        plan = SweepPlan(weights, grid, n, device=dev, with_matrix=True, kernel=args.kernel)
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):
-            for _ in range(2):
-                plan.launch(d_f, d_b)
-        torch.cuda.current_stream(dev).wait_stream(side)
-        torch.cuda.synchronize(dev)
-        # two captures of the same step: with the kernel events (every
-        # --event-every'th timed step: the dominant kernel's own duration) and
-        # without (an event between two kernels costs the graph its launch
-        # overlap, a few us per boundary)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            plan.launch(d_f, d_b, (ev_s, ev_e))
-        graph_plain = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph_plain):
-            plan.launch(d_f, d_b)
-        step = graph.replay
-        step_plain = graph_plain.replay
-        launches_per_step = plan.launches_per_run
-        units_local = P * upp
-    else:
-        from paper_2405_03831_b200.dist import ShardedSweep
-        sh = ShardedSweep(weights, grid, n, device=dev, kernel=args.kernel)
-        plan = sh.plan
-        for _ in range(2):
-            sh.run(d_f, d_b)
-        torch.cuda.synchronize(dev)
-        ref_m = sh.matrix.clone()
+    sh = ShardedSweep(weights, grid, n, device=dev, kernel=args.kernel)
+    plan = sh.plan
+    eps = sh.run_checked(d_f, d_b)
+    sh.run(d_f, d_b, rel_eps=eps)
+    torch.cuda.synchronize(dev)
+    ref_m = sh.matrix.clone() if sh.is_root else None
 
-        def step():
-            sh.run(d_f, d_b, (ev_s, ev_e))
-        step_plain = None
-        graph_mode = "eager"
-        if dist.get_backend() == "nccl" and not os.environ.get("COSCHED_NO_GRAPH"):
-            # the whole step -- shard sweep, NCCL all-gather, device scatter -- as
-            # one CUDA graph; kept only if its replay reproduces the eager matrix
-            try:
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    sh.run(d_f, d_b, (ev_s, ev_e))
+    def step():
+        sh.run(d_f, d_b, (ev_s, ev_e), rel_eps=eps)
+    graph_mode = "eager"
+    if dist.get_backend() == "nccl" and not os.environ.get("COSCHED_NO_GRAPH"):
+        # the whole step -- shard sweep, pack, NCCL gather, rank-0 rebuild -- as
+        # one CUDA graph; kept only if its replay reproduces the eager matrix
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                sh.run(d_f, d_b, (ev_s, ev_e), rel_eps=eps)
+            if sh.is_root:
                 sh.matrix.zero_()
-                g.replay()
-                torch.cuda.synchronize(dev)
-                ok = torch.tensor([int(torch.equal(sh.matrix, ref_m))], device=dev)
-                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-                if int(ok) == 1:
-                    step, graph_mode = g.replay, "cuda-graph (sweep + NCCL all-gather + scatter)"
-                    step_plain = None
-            except Exception as exc:   # capture unsupported here: stay eager
-                print(f"rank {rank}: graph capture failed ({exc}); eager steps", file=sys.stderr)
-                torch.cuda.synchronize(dev)
-        launches_per_step = plan.launches_per_run + 1   # + cs_scatter_gathered
-        units_local = plan.P * upp
-
+            g.replay()
+            torch.cuda.synchronize(dev)
+            ok = torch.tensor([int(torch.equal(sh.matrix, ref_m)) if sh.is_root else 1], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok) == 1:
+                step, graph_mode = g.replay, "cuda-graph (sweep + pack + NCCL gather + rank-0 rebuild)"
+        except Exception as exc:   # capture unsupported here: stay eager
+            print(f"rank {rank}: graph capture failed ({exc}); eager steps", file=sys.stderr)
+            torch.cuda.synchronize(dev)
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize(dev)
-    c = plan.read_counters()
+    err, bad = sh.status()
 
-    # ---------------- timed region ----------------
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms, sweep_ms = [], []
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(local_rank) as clk:
         t_wall = time.perf_counter()
         for k in range(args.steps):
-            flush.zero_()                       # L2 flush, outside the step events
-            sample = step_plain is None or k % args.event_every == 0
+            flush.zero_()
             st.record()
-            (step if sample else step_plain)()
+            step()
             en.record()
             en.synchronize()
             step_ms.append(st.elapsed_time(en))
-            if sample:
-                sweep_ms.append(ev_s.elapsed_time(ev_e))
+            sweep_ms.append(ev_s.elapsed_time(ev_e))
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t_wall
-    if world > 1:
-        dist.barrier()
-    total_ms = float(sum(step_ms))
-    sweep_avg = float(np.mean(sweep_ms))
-    if world > 1:
-        t = torch.tensor([total_ms, sweep_avg], dtype=torch.float64,
-                         device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, sweep_avg = float(t[0]), float(t[1])
-    value = P * upp * args.steps / (total_ms / 1e3)
-
+    dist.barrier()
+    t = torch.tensor([float(sum(step_ms)), float(np.mean(sweep_ms))], dtype=torch.float64,
+                     device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, sweep_avg = float(t[0]), float(t[1])
+    units = P * grid.n_grid
     result = None
     if rank == 0:
-        tf, hbm, src = measured_peaks()
-        achieved_tflops = FLOPS_PER_UNIT * units_local / (sweep_avg / 1e3) / 1e12
+        ms = total_ms / args.steps
         result = {
-            "metric": "(pair,knob) configs evaluated/sec", "value": value, "unit": "configs/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "metric": "(pair,knob) configs evaluated/sec", "value": units * args.steps / (total_ms / 1e3),
+            "value_reference_equivalent": P * grid.units_per_pair() * args.steps / (total_ms / 1e3),
+            "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp32 screen / fp64 exact re-evaluation",
             "data": "synthetic: simenv-equivalent workload (seed 0) + acceptance-recipe trained weights",
-            "config": {"workload": WORKLOADS[args.workload][3], "n_apps": n, "pairs": P,
-                       "configs_per_pair": upp, "budgets": [s.p_total for s in spaces],
-                       "l2": "flushed before every step (256 MiB memset, outside the events)",
-                       "kernel_events": (f"sweep kernel timed on every {args.event_every}th step "
-                                         "(same graph + 2 events)" if world == 1 else "every step"),
-                       "step": ("CUDA graph: k_tables (+solo splits) -> k_sweep_tc3 (+decide, "
-                                "scatter) -> k_resolve (+decide)" if world == 1 else
-                                "shard sweep (3 kernels) -> ONE all-gather of the packed pair "
-                                f"records -> device scatter of the full matrix; {graph_mode}"),
-                       "parallelism": f"pair shards x{world}"},
-            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tf,
-                         "unit": "TFLOP/s", "frac": achieved_tflops / tf,
-                         "traffic": measured_traffic(args.workload, args.kernel),
-                         "kernel": {"tcgen05": "k_sweep_tc3<L,4,2,3> (tcgen05, A in TMEM, v4)",
-                                    "simt": "k_sweep (SIMT fp32)"}[args.kernel], "kernel_ms": sweep_avg,
-                         "flops_per_unit": FLOPS_PER_UNIT, "units_per_launch": units_local,
-                         "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
-                         "kernel_share_of_step": sweep_avg / (total_ms / args.steps)},
-            "roofline_issue": issue_roofline(args, sweep_avg, world),
-            "gpu_launches": launches_per_step * args.steps,
+            "config": bench_config(name, n, grid, world),
+            "method": {"l2": "flushed before every step (256 MiB memset, outside the events)",
+                       "step": f"shard sweep (3 kernels) -> pack 11-B records -> ONE NCCL gather "
+                               f"to rank 0 -> rank-0 device rebuild of records + matrix; {graph_mode}",
+                       "timing": "CUDA events per rank, max over ranks"},
+            "roofline": roofline(name, args.kernel, sweep_avg, plan.P * grid.n_grid, ms),
+            "gpu_launches": (plan.launches_per_run + 1 + (1 if sh.is_root else 0)) * args.steps,
             "clocks": clk.summary(),
-            "screen": {"queue_len": c.queue_len, "max_rel_gap": c.screen_error},
+            "screen": {"max_rel_gap_all_ranks": err, "verify_fail_any_rank": bad},
             "wall_s_timed_region": wall,
         }
-    # ---------------- e2e: host buffers in, result matrix out ----------------
-    if world > 1 and not args.no_e2e:
-        # every rank: pinned features -> H2D -> its shard -> NCCL all-gather ->
-        # full matrix; rank 0 reads the matrix back (the host matcher's input)
+    if not args.no_e2e:
+        # every rank: pinned features -> H2D -> its shard -> gather -> rank 0's
+        # matrix read back (the host matcher's input); checked each call
         h_f = torch.from_numpy(np.ascontiguousarray(F)).pin_memory()
         h_b = torch.from_numpy(np.ascontiguousarray(T)).pin_memory()
         h_m = torch.empty((grid.n_budgets, n, n), dtype=torch.float64).pin_memory() \
             if rank == 0 else None
         for _ in range(2):
             sh.run_host(h_f, h_b, h_m)
-        k = max(3, min(args.steps, 50))
+        k = max(3, min(args.steps, 20))
         dist.barrier()
         t0 = time.perf_counter()
         for _ in range(k):
@@ -502,68 +737,15 @@ def run_ours(args):
                           device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         if rank == 0:
-            result["e2e"] = {"value": P * upp / float(tt[0]), "unit": "configs/s",
+            result["e2e"] = {"value": units / float(tt[0]), "unit": "configs/s",
                              "h2d_bytes_per_step": (F.nbytes + T.nbytes) * world,
-                             "d2h_bytes_per_step": h_m.numel() * 8, "steps": k, "n_apps": n,
-                             "api": "dist.ShardedSweep.run_host (pinned host in, NCCL all-gather, "
-                                    "matrix D2H on rank 0; max over ranks)"}
-    if world == 1 and not args.no_e2e:
-        from paper_2405_03831_b200.host_abi import HostGraphCall
-        from paper_2405_03831_b200 import matcher, scheduler
-        n1, sp1 = spaces_for(args.workload)
-        g1 = KnobGrid(sp1)
-        F1, T1 = synth.workload_arrays(0, synth.mixed_archetypes(n1))
-        # the step's result is the weight matrix the matcher consumes (+ solo splits);
-        # the per-pair records stay on the device
-        call = HostGraphCall(weights, g1, n1, device=dev, with_records=False)
-        call.h_features[...] = F1
-        call.h_base_time[...] = T1
-        for _ in range(max(2, args.warmup)):
-            call()
-        k = max(3, min(args.steps, 200))
-        ts = []
-        for _ in range(k):
-            t0 = time.perf_counter()
-            call()
-            ts.append(time.perf_counter() - t0)
-        h2d, d2h = call.bytes_per_call()
-        P1 = n1 * (n1 - 1) // 2
-        e2e_val = P1 * g1.units_per_pair() / float(np.mean(ts))
-        result["e2e"] = {"value": e2e_val, "unit": "configs/s", "h2d_bytes_per_step": h2d,
-                         "d2h_bytes_per_step": d2h, "steps": k, "n_apps": n1,
-                         "api": "cs_build_graph_host (C ABI, pinned host buffers; D2H = N x N weights + "
-                                "solo times/splits + clamps)"}
-        # second BASELINE metric: schedule time at this N (sweep + D2H + host matching)
-        jobs = synth.generate_jobs(0, synth.mixed_archetypes(n1))
-        from paper_2405_03831_b200 import core as _core
-        inp = scheduler.SchedulerInput(tuple(jobs), sp1[-1], _core.SchedulingParams(window=n1),
-                                       weights)
-        if n1 <= 4096:
-            # HardwareConfig validates caps against the module constants
-            # (core.py:121-128 in the reference): a non-default cap grid needs
-            # them patched, exactly as the reference's own oracle run does
-            saved = (_core.CPU_CAPS, _core.GPU_CAPS)
-            _core.CPU_CAPS, _core.GPU_CAPS = sp1[-1].cpu_caps, sp1[-1].gpu_caps
-            try:
-                scheduler.build_graph(inp)            # warm (plan cache, GPU path)
-                t0 = time.perf_counter()
-                graph = scheduler.build_graph(inp)
-                t1 = time.perf_counter()
-                matched = matcher.min_weight_perfect_matching(graph)
-                t2 = time.perf_counter()
-                scheduler.emit_schedule(inp, graph, matched)
-                t3 = time.perf_counter()
-            finally:
-                _core.CPU_CAPS, _core.GPU_CAPS = saved
-            result["schedule_e2e_s"] = {"total": t3 - t0, "build_graph": t1 - t0,
-                                        "matching": t2 - t1, "emit": t3 - t2, "n_apps": n1}
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
-        result["cpu_baseline"] = cpu_baseline(weights, args.workload, seconds=args.cpu_seconds)
+                             "d2h_bytes_per_step": h_m.numel() * 8, "steps": k,
+                             "api": "dist.ShardedSweep.run_host (pinned host in, NCCL gather to "
+                                    "rank 0, matrix D2H on rank 0; max over ranks)"}
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():
@@ -571,12 +753,15 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--workload", default="n256", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: n256 on 1 GPU (plus n4096 / n1024x5 sub-results), "
+                         "n4096 strong-scaled on N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="tcgen05", choices=["tcgen05", "simt"],
                     help="screen kernel of the pair sweep (results are identical)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-subresults", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--event-every", type=int, default=16,
                     help="time the dominant kernel with CUDA events on every k-th timed step "

@@ -262,16 +262,24 @@ int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begi
                        int64_t pair_end, double *d_w, void *stream);
 
 /* --- multi-GPU record exchange (dist.py) -------------------------------- *
- * A rank's pair records packed into ONE buffer (cap pairs per budget): weight
- * f64 | corun_time f64 | corun_grid_index i32 | corun_chosen u8, each field
- * budget-major with the rank's own pair count as row stride, 256-B aligned.
- * Every rank's buffer has the same size, so one NCCL all-gather moves them
- * all; cs_scatter_gathered then writes the symmetric L x N x N matrix from the
- * gathered blocks (rank r owns pairs dist.shard_range(P, r, world)). */
-size_t cs_packed_records_bytes(int64_t cap, int32_t n_budgets);
-int cs_packed_records_layout(void *d_base, int64_t cap, int32_t n_budgets, cs_pair_out *out);
-int cs_scatter_gathered(const void *d_gathered, int32_t world, size_t rec_bytes, int64_t n_pairs,
-                        int32_t n_apps, int32_t n_budgets, double *d_w, void *stream);
+ * The wire format of one rank's shard: 11 bytes per (pair, budget) --
+ * corun_time f64 | corun_grid_index u16 (0xFFFF: none) | corun_chosen u8 --
+ * each field budget-major with `cap` slots per budget, 256-B aligned.  The
+ * winning weight is not sent: rank 0 re-derives it exactly as the sweep does
+ * (co-run time if chosen, else (0.0 + t_i) + t_j, hwopt.py:39-41).  Every
+ * rank's buffer has the same size, so one NCCL gather to rank 0 moves them
+ * all (rank r owns pairs dist.shard_range(P, r, world)). */
+size_t cs_wire_records_bytes(int64_t cap, int32_t n_budgets);
+/* shard records (cs_pair_out with row stride n_pairs) -> wire buffer */
+int cs_pack_records(cs_pair_out shard, int64_t n_pairs, int32_t n_budgets, int64_t cap,
+                    void *d_wire, void *stream);
+/* rank 0: the `world` gathered wire buffers (wire_bytes each, rank order) ->
+ * the full record set `full` (L x P, P = N(N-1)/2; weight re-derived from
+ * d_solo_time, L x N) and, when d_w is not NULL, the symmetric L x N x N
+ * matrix (diagonal left untouched: zero it once). */
+int cs_unpack_gathered(const void *d_gathered, int32_t world, size_t wire_bytes, int32_t n_apps,
+                       int32_t n_budgets, const double *d_solo_time, cs_pair_out full,
+                       double *d_w, void *stream);
 
 /* The pair sweep with the reference's ANALYTIC oracle as the model
  * (simenv.py:154-233) instead of the FNN.  The caller

@@ -133,12 +133,12 @@ SWEEP_SYMBOLS = {
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_scatter_weights": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
-    "cs_packed_records_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32]),
-    "cs_packed_records_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
-                                                ctypes.POINTER(CsPairOut)]),
-    "cs_scatter_gathered": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t,
-                                           ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
-                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_wire_records_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32]),
+    "cs_pack_records": (ctypes.c_int, [CsPairOut, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_unpack_gathered": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                          CsPairOut, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_analytic_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, c_double_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,

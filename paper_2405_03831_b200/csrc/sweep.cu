@@ -883,29 +883,73 @@ __global__ void k_scatter(const double *__restrict__ weight, int n, int64_t p_be
     }
 }
 
-// ---- k_scatter_gathered: the full matrix from an all-gathered record set ----
-// Rank r's block (rec_bytes each, world blocks back to back) holds its pair
-// shard dist.shard_range(P, r, world) in the packed layout of
-// cs_packed_records_layout: weight f64 [L][P_r] at offset 0, then the other
-// fields (unused here).  One thread per global pair.
-__global__ void k_scatter_gathered(const uint8_t *__restrict__ gathered, int world, int64_t rec_bytes,
-                                   int64_t P, int n, int L, double *__restrict__ W) {
+// ---- multi-GPU wire records (cs_pack_records / cs_unpack_gathered) --------
+struct WireLayout {
+    size_t time, idx, flag, total;
+};
+__host__ __device__ __forceinline__ size_t wire_align(size_t v) { return (v + 255) & ~(size_t)255; }
+__host__ __device__ __forceinline__ WireLayout wire_layout(int64_t cap, int L) {
+    WireLayout w;
+    const size_t n = (size_t)cap * L;
+    w.time = 0;
+    w.idx = wire_align(8 * n);
+    w.flag = w.idx + wire_align(2 * n);
+    w.total = w.flag + wire_align(n);
+    return w;
+}
+
+__global__ void k_pack_records(const cs_pair_out shard, int64_t P, int L, int64_t cap,
+                               uint8_t *__restrict__ wire) {
+    const WireLayout w = wire_layout(cap, L);
+    double *t = reinterpret_cast<double *>(wire + w.time);
+    uint16_t *ix = reinterpret_cast<uint16_t *>(wire + w.idx);
+    uint8_t *fl = wire + w.flag;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)L * P;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = e / P, p = e - l * P, o = l * cap + p;
+        const int32_t g = shard.corun_grid_index[e];
+        t[o] = shard.corun_time[e];
+        ix[o] = g < 0 ? (uint16_t)0xFFFF : (uint16_t)g;
+        fl[o] = shard.corun_chosen[e];
+    }
+}
+
+// One thread per global pair: owner rank of pair p, its wire slot, the
+// decision record and (optionally) the two matrix entries, every budget.
+__global__ void k_unpack_gathered(const uint8_t *__restrict__ gathered, int world, int64_t wire_bytes,
+                                  int64_t P, int n, int L, int64_t cap,
+                                  const double *__restrict__ solo_time, const cs_pair_out full,
+                                  double *__restrict__ W) {
     const int64_t base = P / world, extra = P % world;
+    const WireLayout wl = wire_layout(cap, L);
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         // owner rank of pair p: the first `extra` ranks hold base + 1 pairs
         const int64_t cut = extra * (base + 1);
         const int64_t r = p < cut ? p / (base + 1) : extra + (p - cut) / base;
         const int64_t b = r * base + (r < extra ? r : extra);
-        const int64_t Pr = base + (r < extra ? 1 : 0);
-        const double *w = reinterpret_cast<const double *>(gathered + r * rec_bytes);
+        const uint8_t *blk = gathered + r * wire_bytes;
+        const double *t = reinterpret_cast<const double *>(blk + wl.time);
+        const uint16_t *ix = reinterpret_cast<const uint16_t *>(blk + wl.idx);
+        const uint8_t *fl = blk + wl.flag;
         int i, j;
         pair_of(p, n, i, j);
         for (int l = 0; l < L; ++l) {
-            const double v = w[(int64_t)l * Pr + (p - b)];
-            double *Wl = W + (size_t)l * n * n;
-            Wl[(size_t)i * n + j] = v;
-            Wl[(size_t)j * n + i] = v;
+            const int64_t s = (int64_t)l * cap + (p - b), o = (int64_t)l * P + p;
+            const double co = t[s];
+            const uint16_t g = ix[s];
+            const bool chosen = fl[s] != 0;
+            const double *st = solo_time + (size_t)l * n;
+            const double w = chosen ? co : (0.0 + st[i]) + st[j];     // hwopt.py:39-41
+            full.corun_grid_index[o] = g == 0xFFFF ? -1 : (int32_t)g;
+            full.corun_time[o] = co;
+            full.corun_chosen[o] = chosen;
+            full.weight[o] = w;
+            if (W) {
+                double *Wl = W + (size_t)l * n * n;
+                Wl[(size_t)i * n + j] = w;
+                Wl[(size_t)j * n + i] = w;
+            }
         }
     }
 }
@@ -1568,36 +1612,39 @@ int cs_scatter_weights(const double *d_weight, int32_t n_apps, int64_t pair_begi
     return check_launch();
 }
 
-size_t cs_packed_records_bytes(int64_t cap, int32_t n_budgets) {
+size_t cs_wire_records_bytes(int64_t cap, int32_t n_budgets) {
     if (cap < 0 || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS) return 0;
-    const size_t n = (size_t)cap * n_budgets;
-    return align256(8 * n) * 2 + align256(4 * n) + align256(n);
+    return wire_layout(cap, n_budgets).total;
 }
 
-int cs_packed_records_layout(void *d_base, int64_t cap, int32_t n_budgets, cs_pair_out *out) {
-    if (!d_base || !out || ((uintptr_t)d_base & 255) || !cs_packed_records_bytes(cap, n_budgets))
+int cs_pack_records(cs_pair_out shard, int64_t n_pairs, int32_t n_budgets, int64_t cap,
+                    void *d_wire, void *stream) {
+    if (!d_wire || n_pairs < 0 || cap < n_pairs || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS ||
+        !shard.corun_grid_index || !shard.corun_time || !shard.corun_chosen || ((uintptr_t)d_wire & 255))
         return CS_ERR_ARG;
-    const size_t n = (size_t)cap * n_budgets;
-    char *p = (char *)d_base;
-    out->weight = (double *)p;
-    p += align256(8 * n);
-    out->corun_time = (double *)p;
-    p += align256(8 * n);
-    out->corun_grid_index = (int32_t *)p;
-    p += align256(4 * n);
-    out->corun_chosen = (uint8_t *)p;
-    return CS_OK;
-}
-
-int cs_scatter_gathered(const void *d_gathered, int32_t world, size_t rec_bytes, int64_t n_pairs,
-                        int32_t n_apps, int32_t n_budgets, double *d_w, void *stream) {
-    if (!d_gathered || !d_w || world < 1 || n_apps < 2 ||
-        n_pairs != (int64_t)n_apps * (n_apps - 1) / 2 || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS)
-        return CS_ERR_ARG;
-    int64_t blocks = (n_pairs + 255) / 256;
+    if (!n_pairs) return CS_OK;
+    int64_t blocks = ((int64_t)n_budgets * n_pairs + 255) / 256;
     if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
-    k_scatter_gathered<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        (const uint8_t *)d_gathered, world, (int64_t)rec_bytes, n_pairs, n_apps, n_budgets, d_w);
+    k_pack_records<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(shard, n_pairs, n_budgets, cap,
+                                                                       (uint8_t *)d_wire);
+    return check_launch();
+}
+
+int cs_unpack_gathered(const void *d_gathered, int32_t world, size_t wire_bytes, int32_t n_apps,
+                       int32_t n_budgets, const double *d_solo_time, cs_pair_out full,
+                       double *d_w, void *stream) {
+    if (!d_gathered || world < 1 || n_apps < 2 || n_budgets < 1 || n_budgets > CS_MAX_BUDGETS ||
+        !d_solo_time || !full.corun_grid_index || !full.corun_time || !full.corun_chosen ||
+        !full.weight)
+        return CS_ERR_ARG;
+    const int64_t P = (int64_t)n_apps * (n_apps - 1) / 2;
+    const int64_t cap = (P + world - 1) / world;
+    if (wire_bytes != wire_layout(cap, n_budgets).total) return CS_ERR_ARG;
+    int64_t blocks = (P + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+    k_unpack_gathered<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        (const uint8_t *)d_gathered, world, (int64_t)wire_bytes, P, n_apps, n_budgets, cap,
+        d_solo_time, full, d_w);
     return check_launch();
 }
 

@@ -126,11 +126,7 @@ class SweepPlan:
 
     def __init__(self, weights, grid: KnobGrid, n: int, pair_begin: int = 0,
                  pair_end: Optional[int] = None, device=None, with_matrix: bool = True,
-                 rel_eps: float = DEFAULT_REL_EPS, kernel: str = "tcgen05",
-                 record_cap: Optional[int] = None):
-        """record_cap: carve the per-pair records from ONE packed buffer sized for
-        `record_cap` pairs per budget (cs_packed_records_layout), so a multi-GPU
-        run all-gathers every field with a single collective (dist.py)."""
+                 rel_eps: float = DEFAULT_REL_EPS, kernel: str = "tcgen05"):
         self.lib = nat.sweep_lib()
         self.device = require_cuda(device)
         if n < 2:
@@ -167,28 +163,10 @@ class SweepPlan:
             nat.check(self.lib.cs_tables_set_network(self.net.ref(), ctypes.byref(self.tables),
                                                      _stream_handle(dev)), "cs_tables_set_network")
             P = max(self.P, 1)
-            if record_cap is None:
-                self.records = None
-                self.corun_grid_index = torch.empty((L, P), dtype=torch.int32, device=dev)
-                self.corun_time = torch.empty((L, P), dtype=torch.float64, device=dev)
-                self.corun_chosen = torch.empty((L, P), dtype=torch.uint8, device=dev)
-                self.weight = torch.empty((L, P), dtype=torch.float64, device=dev)
-            else:
-                if record_cap < self.P:
-                    raise ValidationError(f"record_cap {record_cap} < shard size {self.P}")
-                rb = self.lib.cs_packed_records_bytes(record_cap, L)
-                self.records = torch.zeros(rb, dtype=torch.uint8, device=dev)
-                lay = nat.CsPairOut()
-                nat.check(self.lib.cs_packed_records_layout(_dptr(self.records), record_cap, L,
-                                                            ctypes.byref(lay)),
-                          "cs_packed_records_layout")
-                base = _dptr(self.records)
-                view = lambda ptr, dt, es: self.records[ctypes.cast(ptr, ctypes.c_void_p).value - base:][
-                    :L * P * es].view(dt).view(L, P)
-                self.weight = view(lay.weight, torch.float64, 8)
-                self.corun_time = view(lay.corun_time, torch.float64, 8)
-                self.corun_grid_index = view(lay.corun_grid_index, torch.int32, 4)
-                self.corun_chosen = view(lay.corun_chosen, torch.uint8, 1)
+            self.corun_grid_index = torch.empty((L, P), dtype=torch.int32, device=dev)
+            self.corun_time = torch.empty((L, P), dtype=torch.float64, device=dev)
+            self.corun_chosen = torch.empty((L, P), dtype=torch.uint8, device=dev)
+            self.weight = torch.empty((L, P), dtype=torch.float64, device=dev)
             self.solo_time = torch.empty((L, n), dtype=torch.float64, device=dev)
             self.solo_split = torch.empty((L, n), dtype=torch.int32, device=dev)
             self.solo_clamps = torch.empty((L, n), dtype=torch.int32, device=dev)

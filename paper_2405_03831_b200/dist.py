@@ -1,13 +1,23 @@
-"""Multi-GPU sweep: pairs sharded across ranks, one all-gather of the records.
+"""Multi-GPU sweep: pairs sharded across ranks, one gather of 11-byte records to rank 0.
 
 One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch for the
 data path).  Pairs are independent units, so rank r sweeps the
 contiguous linear pair range ``shard_range(P, r, W)`` with the per-app and
 per-knob tables replicated (each rank builds its own; they are ~N*37 floats).
-The only exchange is the all-gather of the fixed-size per-pair records
-(best config index i32, CoRunTime f64, co-run flag u8, winning weight f64),
-after which every rank holds the full record set; the scatter into the
-symmetric N x N matrix that the host matcher consumes runs on the device.
+
+The only exchange is ONE gather to rank 0 -- the host matcher runs there --
+of each shard's decision records in the 11-byte wire format of
+``cs_pack_records`` (CoRunTime f64, config index u16, co-run flag u8 per
+(pair, budget)).  Rank 0 rebuilds the full record set and the symmetric
+N x N matrix on its device (``cs_unpack_gathered``, which re-derives each
+winning weight exactly as the sweep does).  At 4,096 apps that is 92 MB
+in total over NVSwitch, against 176 MB of 21-byte records all-gathered to
+every rank before.
+
+Exactness is a collective property: after each run the ranks all-reduce
+(MAX) their screen-error monitor and their sampled re-scan disagreements;
+should either call for a wider ambiguity band, every rank redoes its shard
+with the same wider band (the rule of ``sweep.run_plan``).
 """
 
 from __future__ import annotations
@@ -16,9 +26,6 @@ from typing import Optional
 
 import torch
 import torch.distributed as dist
-
-RECORD_FIELDS = (("corun_grid_index", torch.int32), ("corun_time", torch.float64),
-                 ("corun_chosen", torch.uint8), ("weight", torch.float64))
 
 
 def shard_range(P: int, rank: int, world: int) -> tuple:
@@ -30,39 +37,40 @@ def shard_range(P: int, rank: int, world: int) -> tuple:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
-def gather_records(local: dict, P: int, group: Optional[dist.ProcessGroup] = None) -> dict:
-    """All-gather per-rank record shards (each (L, P_rank)) into full (L, P) tensors.
+def shard_cap(P: int, world: int) -> int:
+    """Slots per budget of every rank's wire buffer (the largest shard)."""
+    return (P + world - 1) // world if world else 0
 
-    Shards are padded to the largest shard so one ``all_gather_into_tensor``
-    per field suffices (NCCL's ring/NVLS all-gather needs equal sizes); the
-    padding is dropped while re-assembling in rank order.
-    """
+
+def wire_layout(cap: int, L: int) -> dict:
+    """Byte offsets of the wire fields (mirrors cs_wire_records_bytes)."""
+    a = lambda v: (v + 255) & ~255
+    n = cap * L
+    t, i = 0, a(8 * n)
+    f = i + a(2 * n)
+    return {"corun_time": t, "corun_grid_index": i, "corun_chosen": f, "total": f + a(n)}
+
+
+def gather_to_root(local: torch.Tensor, group: Optional[dist.ProcessGroup] = None,
+                   root: int = 0) -> Optional[torch.Tensor]:
+    """Gather every rank's equal-sized uint8 buffer to `root`: a (world, nbytes)
+    tensor there, None elsewhere.  NCCL for CUDA buffers (one gather over
+    NVLink); gloo (CPU tests, ranks sharing one GPU) through host memory."""
     world = dist.get_world_size(group)
-    sizes = [shard_range(P, r, world) for r in range(world)]
-    cap = max(e - b for b, e in sizes)
-    out = {}
-    for name, dtype in RECORD_FIELDS:
-        t = local[name]
-        L, n_local = t.shape
-        padded = torch.zeros((L, cap), dtype=dtype, device=t.device)
-        padded[:, :n_local] = t
-        # gather buffer laid out rank-major: (world, L, cap)
-        buf = torch.empty((world, L, cap), dtype=dtype, device=t.device)
-        if t.device.type == "cuda" and dist.get_backend(group) == "nccl":
-            dist.all_gather_into_tensor(buf, padded.contiguous(), group=group)
-        else:   # gloo (CPU tests, or ranks sharing one GPU): stage through the host
-            host = [torch.empty((L, cap), dtype=dtype) for _ in range(world)]
-            dist.all_gather(host, padded.cpu().contiguous(), group=group)
-            buf.copy_(torch.stack(host))
-        full = torch.empty((L, P), dtype=dtype, device=t.device)
-        for r, (b, e) in enumerate(sizes):
-            full[:, b:e] = buf[r, :, :e - b]
-        out[name] = full
+    rank = dist.get_rank(group)
+    nccl = local.device.type == "cuda" and dist.get_backend(group) == "nccl"
+    src = local if nccl else local.cpu()
+    out = torch.empty((world, local.numel()), dtype=torch.uint8, device=src.device) \
+        if rank == root else None
+    dist.gather(src, list(out.unbind(0)) if out is not None else None,
+                dst=dist.get_global_rank(group, root) if group is not None else root, group=group)
+    if out is not None and out.device != local.device:
+        out = out.to(local.device)
     return out
 
 
 class ShardedSweep:
-    """A SweepPlan on this rank's pair shard plus the gather and the device scatter."""
+    """A SweepPlan on this rank's pair shard, the record gather and rank 0's rebuild."""
 
     def __init__(self, weights, grid, n: int, group=None, device=None, rel_eps=None,
                  kernel: str = "tcgen05"):
@@ -72,82 +80,94 @@ class ShardedSweep:
         self.world = dist.get_world_size(group)
         self.n = n
         self.P = n * (n - 1) // 2
+        self.L = grid.n_budgets
         b, e = shard_range(self.P, self.rank, self.world)
-        cap = max(e2 - b2 for b2, e2 in (shard_range(self.P, r, self.world)
-                                         for r in range(self.world)))
-        # the shard's records live in one packed buffer of the same size on every
-        # rank: the exchange is ONE all-gather (NCCL over NVLink), then one device
-        # scatter of the whole matrix from the gathered blocks
+        self.cap = shard_cap(self.P, self.world)
         self.plan = SweepPlan(weights, grid, n, b, e, device=device, with_matrix=False,
                               rel_eps=DEFAULT_REL_EPS if rel_eps is None else rel_eps,
-                              kernel=kernel, record_cap=cap)
-        self.cap = cap
-        self.gathered = torch.empty(self.world * self.plan.records.numel(), dtype=torch.uint8,
-                                    device=self.plan.device)
-        self.matrix = torch.zeros((grid.n_budgets, n, n), dtype=torch.float64,
-                                  device=self.plan.device)
-
-    def run_host(self, h_features, h_base_time, h_matrix=None) -> None:
-        """End to end on this rank: pinned host inputs -> H2D -> shard sweep ->
-        all-gather -> full matrix -> D2H into `h_matrix` (pinned, rank 0 only
-        needs it; pass None elsewhere).  Synchronizes the stream."""
+                              kernel=kernel)
         dev = self.plan.device
-        d_f = h_features.to(dev, non_blocking=True)
-        d_b = h_base_time.to(dev, non_blocking=True)
-        full = self.run(d_f, d_b)
-        if h_matrix is not None:
-            h_matrix.copy_(full, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
+        self.wire_bytes = int(self.plan.lib.cs_wire_records_bytes(self.cap, self.L))
+        self.wire = torch.zeros(self.wire_bytes, dtype=torch.uint8, device=dev)
+        self.is_root = self.rank == 0
+        self.gathered = None
+        if self.is_root:
+            # the full record set and matrix live on rank 0 only
+            self.full = {"corun_grid_index": torch.empty((self.L, self.P), dtype=torch.int32, device=dev),
+                         "corun_time": torch.empty((self.L, self.P), dtype=torch.float64, device=dev),
+                         "corun_chosen": torch.empty((self.L, self.P), dtype=torch.uint8, device=dev),
+                         "weight": torch.empty((self.L, self.P), dtype=torch.float64, device=dev)}
+            self.matrix = torch.zeros((self.L, n, n), dtype=torch.float64, device=dev)
+        else:
+            self.full, self.matrix = None, None
+        self._status = torch.zeros(2, dtype=torch.float32, device=dev if self._nccl() else "cpu")
+
+    def _nccl(self) -> bool:
+        return self.plan.device.type == "cuda" and dist.get_backend(self.group) == "nccl"
 
     def exchange(self) -> None:
-        """All-gather the packed records of every shard and scatter the full matrix."""
+        """Pack this shard, gather every shard to rank 0, rebuild records + matrix there."""
         from . import _native as nat
         plan = self.plan
-        local = plan.records
-        if local.device.type == "cuda" and dist.get_backend(self.group) == "nccl":
-            dist.all_gather_into_tensor(self.gathered, local, group=self.group)
-        else:   # gloo (CPU tests, ranks sharing one GPU): stage through the host
-            host = [torch.empty_like(local, device="cpu") for _ in range(self.world)]
-            dist.all_gather(host, local.cpu(), group=self.group)
-            self.gathered.copy_(torch.cat(host))
         st = torch.cuda.current_stream(plan.device).cuda_stream
-        nat.check(plan.lib.cs_scatter_gathered(self.gathered.data_ptr(), self.world,
-                                               local.numel(), self.P, self.n,
-                                               plan.grid.n_budgets, self.matrix.data_ptr(), st),
-                  "cs_scatter_gathered")
+        nat.check(plan.lib.cs_pack_records(plan.pair_out, plan.P, self.L, self.cap,
+                                           self.wire.data_ptr(), st), "cs_pack_records")
+        self.gathered = gather_to_root(self.wire, self.group)
+        if self.is_root:
+            f = self.full
+            full = nat.CsPairOut(*(nat.ctypes.cast(f[k].data_ptr(), t) for k, t in (
+                ("corun_grid_index", nat.c_int32_p), ("corun_time", nat.c_double_p),
+                ("corun_chosen", nat.c_uint8_p), ("weight", nat.c_double_p))))
+            nat.check(plan.lib.cs_unpack_gathered(self.gathered.data_ptr(), self.world,
+                                                  self.wire_bytes, self.n, self.L,
+                                                  plan.solo_time.data_ptr(), full,
+                                                  self.matrix.data_ptr(), st),
+                      "cs_unpack_gathered")
 
-    def run(self, d_features, d_base_time, sweep_events=None) -> torch.Tensor:
-        """Sweep the local shard, exchange, and return the full (L, N, N) matrix."""
-        self.plan.launch(d_features, d_base_time, sweep_events)
+    def run(self, d_features, d_base_time, sweep_events=None, rel_eps=None):
+        """Sweep the local shard and exchange (stream-ordered, no host sync):
+        rank 0's full (L, N, N) matrix, None on the other ranks."""
+        self.plan.launch(d_features, d_base_time, sweep_events, rel_eps=rel_eps)
         self.exchange()
         return self.matrix
 
-    def records(self) -> dict:
-        """Full (L, P) record arrays (host-side reassembly of the gathered blocks)."""
-        plan = self.plan
-        L = plan.grid.n_budgets
-        blocks = self.gathered.view(self.world, -1)
-        out = {k: [] for k in ("corun_grid_index", "corun_time", "corun_chosen", "weight")}
-        for r in range(self.world):
-            b, e = shard_range(self.P, r, self.world)
-            Pr = e - b
-            base = blocks[r]
-            o = nat_layout(plan, self.cap, L)
-            for name, (off, dt, es) in o.items():
-                out[name].append(base[off:off + L * Pr * es].view(dt).view(L, Pr))
-        return {k: torch.cat(v, dim=1) for k, v in out.items()}
+    def status(self) -> tuple:
+        """(largest screen error over all ranks, any sampled re-scan disagreement):
+        one tiny all-reduce; synchronizes."""
+        c = self.plan.read_counters()
+        s = torch.tensor([c.screen_error, float(c.verify_fail)], dtype=torch.float32,
+                         device=self._status.device)
+        dist.all_reduce(s, op=dist.ReduceOp.MAX, group=self.group)
+        return float(s[0]), bool(s[1] > 0)
 
+    def run_checked(self, d_features, d_base_time):
+        """run() plus the collective precision guard: if any rank's screen error is
+        not well inside the band (or a sampled re-scan disagreed), every rank
+        redoes its shard with the same wider band.  Returns the band used."""
+        eps = self.plan.rel_eps
+        self.run(d_features, d_base_time, rel_eps=eps)
+        err, bad = self.status()
+        while (err > 0.25 * eps or bad) and 16.0 * eps < 0.1:
+            eps = min(max(16.0 * eps, 16.0 * err), 0.099)
+            self.run(d_features, d_base_time, rel_eps=eps)
+            err, bad = self.status()
+        if err > 0.25 * eps or bad:
+            raise RuntimeError(f"fp32 screen error {err:.3g} is too close to rel_eps {eps:.3g}; "
+                               "argmin parity is no longer guaranteed")
+        return eps
 
-def nat_layout(plan, cap: int, L: int) -> dict:
-    """Byte offsets of the packed record fields (cs_packed_records_layout)."""
-    import ctypes
-    from . import _native as nat
-    lay = nat.CsPairOut()
-    nat.check(plan.lib.cs_packed_records_layout(plan.records.data_ptr(), cap, L,
-                                                ctypes.byref(lay)), "cs_packed_records_layout")
-    base = plan.records.data_ptr()
-    addr = lambda p: ctypes.cast(p, ctypes.c_void_p).value - base
-    return {"weight": (addr(lay.weight), torch.float64, 8),
-            "corun_time": (addr(lay.corun_time), torch.float64, 8),
-            "corun_grid_index": (addr(lay.corun_grid_index), torch.int32, 4),
-            "corun_chosen": (addr(lay.corun_chosen), torch.uint8, 1)}
+    def run_host(self, h_features, h_base_time, h_matrix=None) -> None:
+        """End to end on this rank: pinned host inputs -> H2D -> shard sweep ->
+        gather -> rank 0 rebuilds the matrix -> D2H into `h_matrix` (pinned, rank
+        0 only).  Checked and synchronizing."""
+        dev = self.plan.device
+        d_f = h_features.to(dev, non_blocking=True)
+        d_b = h_base_time.to(dev, non_blocking=True)
+        self.run_checked(d_f, d_b)
+        if self.is_root and h_matrix is not None:
+            h_matrix.copy_(self.matrix, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    def records(self) -> Optional[dict]:
+        """Rank 0: the full (L, P) record tensors (device); None elsewhere."""
+        return self.full

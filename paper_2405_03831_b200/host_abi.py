@@ -50,7 +50,10 @@ class HostGraphCall:
     """Reusable cs_build_graph_host invocation for `n` apps over `grid`."""
 
     def __init__(self, weights, grid: KnobGrid, n: int, rel_eps: float = DEFAULT_REL_EPS,
-                 with_records: bool = True, device=None):
+                 with_records: bool = True, device=None, pair_weight: bool = True):
+        """with_records: also copy back the per-pair decision records (best
+        config index, its CoRunTime, the co-run flag -- what a Schedule needs);
+        pair_weight: plus the per-pair winning time (it duplicates the matrix)."""
         self.lib = nat.sweep_lib()
         self.device = require_cuda(device)
         grid.check_nonempty()
@@ -75,9 +78,13 @@ class HostGraphCall:
             self._t_idx, self.h_idx = _pinned((L, P), torch.int32)
             self._t_ct, self.h_ct = _pinned((L, P), torch.float64)
             self._t_ch, self.h_ch = _pinned((L, P), torch.uint8)
-            self._t_pw, self.h_pw = _pinned((L, P), torch.float64)
+            if pair_weight:
+                self._t_pw, self.h_pw = _pinned((L, P), torch.float64)
+            else:
+                self.h_pw = None
             self.pairs = nat.CsPairOut(nat.ptr(self.h_idx, nat.c_int32_p), nat.ptr(self.h_ct),
-                                       nat.ptr(self.h_ch, nat.c_uint8_p), nat.ptr(self.h_pw))
+                                       nat.ptr(self.h_ch, nat.c_uint8_p),
+                                       nat.ptr(self.h_pw) if pair_weight else None)
         else:
             self.pairs = nat.CsPairOut()
         self._t_st, self.h_solo_time = _pinned((L, n), torch.float64)
@@ -116,7 +123,9 @@ class HostGraphCall:
         d2h = self.h_weights.nbytes + self.h_solo_time.nbytes + self.h_solo_split.nbytes + \
             self.h_solo_clamps.nbytes + self.h_clamps.nbytes
         if self.with_records:
-            d2h += self.h_idx.nbytes + self.h_ct.nbytes + self.h_ch.nbytes + self.h_pw.nbytes
+            d2h += self.h_idx.nbytes + self.h_ct.nbytes + self.h_ch.nbytes
+            if self.h_pw is not None:
+                d2h += self.h_pw.nbytes
         return h2d, d2h
 
     def __call__(self, features=None, base_time=None) -> dict:
@@ -135,7 +144,9 @@ class HostGraphCall:
                "clamps": self.h_clamps}
         if self.with_records:
             out.update(corun_grid_index=self.h_idx, corun_time=self.h_ct,
-                       corun_chosen=self.h_ch.astype(bool), weight=self.h_pw)
+                       corun_chosen=self.h_ch.view(bool))
+            if self.h_pw is not None:
+                out["weight"] = self.h_pw
         return out
 
 

@@ -1,8 +1,8 @@
 """The sharded multi-rank sweep (dist.ShardedSweep) on one GPU: 2 and 3 ranks share
 cuda:0 over gloo (this environment has one GPU; on 8 GPUs the same code runs one
-rank per GPU over NCCL).  The packed-record all-gather + device scatter must
-rebuild exactly the single-process graph, and the reassembled records must
-equal the fp64 oracle."""
+rank per GPU over NCCL).  The 11-byte wire records gathered to rank 0 and
+rank 0's device rebuild (cs_unpack_gathered) must give exactly the
+single-process graph, and the rebuilt records must equal the fp64 oracle."""
 
 import os
 import socket
@@ -38,9 +38,11 @@ def _worker(rank, world, port, n, out_path):
     grid = KnobGrid([core.default_space(400.0), core.default_space(350.0)])
     sh = ShardedSweep(w, grid, n, device=torch.device("cuda", 0))
     d_f, d_b = to_device_inputs(F, T, sh.plan.device)
-    M = sh.run(d_f, d_b)
+    sh.run_checked(d_f, d_b)
+    M = sh.matrix
     torch.cuda.synchronize()
     rec = sh.records()
+    assert (rank == 0) == (rec is not None) == (M is not None)
     if rank == 0:
         np.savez(out_path, matrix=M.cpu().numpy(), **{k: v.cpu().numpy() for k, v in rec.items()})
     dist.barrier()
@@ -69,3 +71,4 @@ def test_sharded_sweep_rebuilds_the_graph(tmp_path, weights, world):
         assert np.array_equal(got["corun_grid_index"][l], ref["corun_grid_index"][l])
         assert np.array_equal(got["weight"][l], ref["weight"][l])
         assert np.array_equal(got["corun_chosen"][l].astype(bool), ref["corun_chosen"][l])
+        assert np.array_equal(got["corun_time"][l], ref["corun_time"][l])
