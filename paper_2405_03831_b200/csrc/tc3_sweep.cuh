@@ -161,7 +161,9 @@ __device__ __forceinline__ void build_row(const float2 (&p2)[9], uint32_t krow, 
     for (int v = 0; v < 9; ++v) {
         const float2 z = tc2::add2(p2[v], kr[v]);
         const uint32_t hw = tc2::cvt_rz_relu(z.x, z.y);
-        const float2 lo = tc2::sub2(z, tc::unpack_half2(hw));
+        // the residual z - hi straight from the packed halves: one mixed
+        // f16*f16+f32 FMA (FHFMA) per element, no f16->f32 unpack
+        const float2 lo = tc2::residual_h2(hw, z);
         const uint32_t lw = tc2::cvt_rn_relu(lo.x, lo.y);
         if (v < 8) { w[v] = hw; w[8 + v] = lw; }
         else { w[16] = hw; w[17] = lw; }
@@ -179,17 +181,6 @@ __device__ __forceinline__ float2 lds_f32x2(const float *p) {
                  : "=f"(v.x), "=f"(v.y)
                  : "r"((uint32_t)__cvta_generic_to_shared(p)));
     return v;
-}
-
-// y = wo . ReLU(z2) + bo for this thread's row of one config (fp32, FFMA2)
-__device__ __forceinline__ float head_from_tmem(uint32_t taddr, const float2 (&wo2)[9], float bo) {
-    float z[HD];
-    tc::tmem_ld18(taddr, z);
-    float2 y2 = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int o = 0; o < 9; ++o)
-        y2 = tc2::fma2(make_float2(fmaxf(z[2 * o], 0.f), fmaxf(z[2 * o + 1], 0.f)), wo2[o], y2);
-    return (y2.x + y2.y) + bo;
 }
 
 }  // namespace tc3
@@ -244,7 +235,8 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
         k12[(2 * c + 1) * ROW32 + h] = a.t.knob2_32[i];
     }
     for (int i = tid; i < a.g.G; i += kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
-    if (tid <= HD) wo_s[tid] = tid < HD ? net.wo[tid] : net.bo;
+    // 0.5 wo (the |z2| half of the ReLU, see `math`) and bo
+    if (tid <= HD) wo_s[tid] = tid < HD ? 0.5f * net.wo[tid] : net.bo;
     for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += kThreads)
         reinterpret_cast<double *>(net64)[i] = __ldg(a.t.net_image + kImgHeadOff + i);
     tc::fence_proxy_async();
@@ -341,13 +333,16 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; bcl[l] = 0; }
 
             // epilogue of config c from stage s (s compile-time after unrolling)
-            auto math = [&](int c, const float (&z)[HD]) {
-                float2 y2 = make_float2(0.f, 0.f);
+            // y = wo . ReLU(z2) + bo with ReLU(x) = (x + |x|) / 2: the linear
+            // half 0.5 wo . z2 is TMEM column 18 (B row 18 = 0.5 wo^T W2, its
+            // bias 0.5 wo . b2), the other half an FFMA2 chain on |z2| (the
+            // abs is a free operand modifier) -- no FMNMX per element
+            auto math = [&](int c, const float (&z)[HD + 2]) {
+                float2 y2 = make_float2(z[HD], bo);
 #pragma unroll
                 for (int o = 0; o < 9; ++o)
-                    y2 = tc2::fma2(make_float2(fmaxf(z[2 * o], 0.f), fmaxf(z[2 * o + 1], 0.f)),
-                                   wo2[o], y2);
-                const float y = (y2.x + y2.y) + bo;
+                    y2 = tc2::fma2(make_float2(fabsf(z[2 * o]), fabsf(z[2 * o + 1])), wo2[o], y2);
+                const float y = y2.x + y2.y;
                 const int cl = y < 0.5f;
                 mind = fminf(mind, fabsf(y - 0.5f));
                 const float tm = fmaxf(y, 0.5f) * T_self;
@@ -362,14 +357,14 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     }
                 }
             };
-            auto load_d = [&](int s, float (&z)[HD]) {
+            auto load_d = [&](int s, float (&z)[HD + 2]) {
                 if (!C::kNoTensor) tc3::mbar_wait_warp(&dr[s], ph[s]);
                 ph[s] ^= 1u;
                 tc::fence_after();
-                tc::tmem_ld18(td[s], z);
+                tc::tmem_ld20(td[s], z);
             };
             auto epilogue = [&](int c, int s) {
-                float z[HD];
+                float z[HD + 2];
                 load_d(s, z);
                 math(c, z);
             };
@@ -398,7 +393,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 // pipeline: build(0 .. S-1); per c: D(c) -> registers, build(c+S)
                 // into the freed stage, then the math of c
                 auto step = [&](int cc, int s) {
-                    float z[HD];
+                    float z[HD + 2];
                     load_d(s, z);
                     if (cc + S < n_cfg) build(cc + S, s);
                     math(cc, z);

@@ -96,6 +96,23 @@ __device__ __forceinline__ void tmem_ld18(uint32_t taddr, float (&v)[18]) {
     for (int k = 0; k < 18; ++k) v[k] = __uint_as_float(r[k]);
 }
 
+// 20 fp32 columns of this thread's TMEM lane (x16 + x4)
+__device__ __forceinline__ void tmem_ld20(uint32_t taddr, float (&v)[20]) {
+    uint32_t r[20];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19])
+                 : "r"(taddr + 16));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 20; ++k) v[k] = __uint_as_float(r[k]);
+}
+
 __device__ __forceinline__ float2 unpack_half2(uint32_t w) {
     __half2 h = *reinterpret_cast<__half2 *>(&w);
     return __half22float2(h);
@@ -149,6 +166,19 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
     return *reinterpret_cast<float2 *>(&r);
 }
 
+// z - float(h) for the two halves of h (lo half <-> z.x): fma.rn.f32.f16
+// (FHFMA), h * -1 + z, exact when h is z truncated to fp16
+__device__ __forceinline__ float2 residual_h2(uint32_t h, float2 z) {
+    float2 r;
+    asm("{\n\t.reg .f16 a, b, m;\n\t"
+        "mov.b32 {a, b}, %2;\n\t"
+        "mov.b16 m, 0xBC00;\n\t"
+        "fma.rn.f32.f16 %0, a, m, %3;\n\t"
+        "fma.rn.f32.f16 %1, b, m, %4;\n}"
+        : "=f"(r.x), "=f"(r.y) : "r"(h), "f"(z.x), "f"(z.y));
+    return r;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
@@ -178,15 +208,29 @@ __device__ void write_b_slices(const Net64P &net, uint16_t *tile, int idx) {
     const int q = idx / 512, rem = idx % 512, n = rem / 16, kk = rem % 16;
     auto hi_of = [](double x) { return (double)__half2float(__double2half(x)); };
     double v = 0.0;
+    // row 18: 0.5 wo^T W2 (and bias 0.5 wo . b2) -- D column 18 is then the
+    // linear half of the head, 0.5 wo . z2 (see k_sweep_tc3's epilogue)
+    double row[HD], bias;
     if (n < HD) {
-        const double *w = net.w2 + n * HD;
+        for (int k = 0; k < HD; ++k) row[k] = net.w2[n * HD + k];
+        bias = net.b2[n];
+    } else {
+        bias = 0.0;
+        for (int k = 0; k < HD; ++k) row[k] = 0.0;
+        for (int o = 0; o < HD; ++o) {
+            for (int k = 0; k < HD; ++k) row[k] += 0.5 * net.wo[o] * net.w2[o * HD + k];
+            bias += 0.5 * net.wo[o] * net.b2[o];
+        }
+    }
+    if (n <= HD) {
+        const double *w = row;
         if (q == 0) v = hi_of(w[kk]);
         else if (q == 2) v = w[kk] - hi_of(w[kk]);
         else if (q == 1) {
             if (kk == 0 || kk == 2) v = hi_of(w[16]);
             else if (kk == 1 || kk == 3) v = hi_of(w[17]);
-            else if (kk == 4) v = hi_of(net.b2[n]);
-            else if (kk == 5) v = net.b2[n] - hi_of(net.b2[n]);
+            else if (kk == 4) v = hi_of(bias);
+            else if (kk == 5) v = bias - hi_of(bias);
             // k 6-7 meet A column 19 = (hi16, hi17): k_sweep_tc3 so folds the
             // W2lo[:, 16:18] term into this slice
             else if (kk == 6) v = w[16] - hi_of(w[16]);
