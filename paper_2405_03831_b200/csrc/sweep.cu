@@ -625,10 +625,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
     if (live) pair_of(a.p_begin + pl, a.n, i, j);
 
     float best[L], second[L];
-    int idx[L], clamps[L];
+    int idx[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; clamps[l] = 0; }
-    float mind = FLT_MAX;     // closest screened prediction to the 0.5 floor
+    for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; }
+    float miny1 = FLT_MAX, miny2 = FLT_MAX;   // smallest screened prediction per member
 
     if (live) {
         float p1[HD], p2[HD], tmp[HD];
@@ -653,13 +653,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
 #pragma unroll
             for (int h = 0; h < HD; ++h) z[h] += p2[h];
             const float y2 = head32(net, z);
-            const int cl = (y1 < 0.5f) + (y2 < 0.5f);
-            mind = fminf(mind, fminf(fabsf(y1 - 0.5f), fabsf(y2 - 0.5f)));
+            miny1 = fminf(miny1, y1);
+            miny2 = fminf(miny2, y2);
             const float tt = fmaxf(fmaxf(y1, 0.5f) * ti, fmaxf(y2, 0.5f) * tj);
 #pragma unroll
             for (int l = 0; l < L; ++l) {
                 if (L == 1 || ((m >> l) & 1u)) {
-                    clamps[l] += cl;
                     if (tt < best[l]) { second[l] = best[l]; best[l] = tt; idx[l] = c; }
                     else second[l] = fminf(second[l], tt);
                 }
@@ -667,17 +666,19 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
         }
     }
 
-    // a prediction too close to the floor for the screen to count its clamp:
-    // k_resolve re-counts the pair's rows in fp64 (every slice of the pair
-    // drops its screened count; slice 0 queues both members)
+    // Floor clamps (estimator.py:106-109) are never counted from the screen:
+    // a member whose screened predictions (over every slice of the pair) all
+    // lie above 0.5 + tau has none; any other member row is queued and
+    // k_resolve re-counts it in fp64
     {
-        // the pair's slices are adjacent lanes: OR their flags
-        int f = live && mind <= a.tau;
-        for (int off = 1; off < S; off <<= 1) f |= __shfl_xor_sync(0xffffffffu, f, off);
-        if (f) {
-#pragma unroll
-            for (int l = 0; l < L; ++l) clamps[l] = 0;
-            if (s == 0) { push_row(a, pl, 0); push_row(a, pl, 1); }
+        float m1 = miny1, m2 = miny2;
+        for (int off = 1; off < S; off <<= 1) {
+            m1 = fminf(m1, __shfl_xor_sync(0xffffffffu, m1, off));
+            m2 = fminf(m2, __shfl_xor_sync(0xffffffffu, m2, off));
+        }
+        if (live && s == 0) {
+            if (!(m1 > 0.5f + a.tau)) push_row(a, pl, 0);
+            if (!(m2 > 0.5f + a.tau)) push_row(a, pl, 1);
         }
     }
 
@@ -693,8 +694,6 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
             second[l] = fminf(fminf(second[l], os), loser);
             if (other) { best[l] = ob; idx[l] = oi; }
         }
-        int tot = __reduce_add_sync(0xffffffffu, clamps[l]);
-        if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.clamps + l, (unsigned long long)tot);
     }
 
     if (!live || s != 0) return;

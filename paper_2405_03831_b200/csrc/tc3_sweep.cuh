@@ -327,10 +327,10 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             const uint32_t krow = tc::smem_u32(k12 + member * ROW32);   // + c * 2 * ROW32 * 4
 
             float best[L], second[L];
-            float mind = FLT_MAX;          // closest screened prediction to the 0.5 floor
-            int idx[L], bcl[L];
+            float miny = FLT_MAX;          // smallest screened prediction of this row
+            int idx[L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; bcl[l] = 0; }
+            for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; }
 
             // epilogue of config c from stage s (s compile-time after unrolling)
             // y = wo . ReLU(z2) + bo with ReLU(x) = (x + |x|) / 2: the linear
@@ -343,17 +343,22 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 for (int o = 0; o < 9; ++o)
                     y2 = tc2::fma2(make_float2(fabsf(z[2 * o]), fabsf(z[2 * o + 1])), wo2[o], y2);
                 const float y = y2.x + y2.y;
-                const int cl = y < 0.5f;
-                mind = fminf(mind, fabsf(y - 0.5f));
+                miny = fminf(miny, y);
                 const float tm = fmaxf(y, 0.5f) * T_self;
                 const float tt = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
-                const uint32_t m = L == 1 ? 1u : masks[c];
+                if (L == 1) {
+                    if (tt < best[0]) { second[0] = best[0]; best[0] = tt; idx[0] = c; }
+                    else second[0] = fminf(second[0], tt);
+                } else {
+                    // branch-free per budget: a config outside budget l enters as +max
+                    const uint32_t m = masks[c];
 #pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    if (L == 1 || ((m >> l) & 1u)) {
-                        bcl[l] += cl;
-                        if (tt < best[l]) { second[l] = best[l]; best[l] = tt; idx[l] = c; }
-                        else second[l] = fminf(second[l], tt);
+                    for (int l = 0; l < L; ++l) {
+                        const float v = ((m >> l) & 1u) ? tt : FLT_MAX;
+                        const bool lt = v < best[l];
+                        second[l] = lt ? best[l] : fminf(second[l], v);
+                        best[l] = lt ? v : best[l];
+                        idx[l] = lt ? c : idx[l];
                     }
                 }
             };
@@ -430,15 +435,10 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 if (x >= 0 && x < n_cfg) epilogue(x, u % S);
             }
             }
-            // a prediction too close to the floor for the screen to count its
-            // clamp: k_resolve re-counts this row's clamps in fp64 instead
-            if (mind <= a.tau) {
-                if (live) push_row(a, pl, member);
-#pragma unroll
-                for (int l = 0; l < L; ++l) bcl[l] = 0;
-            }
-#pragma unroll
-            for (int l = 0; l < L; ++l) clamps[l] += live ? bcl[l] : 0;
+            // Floor clamps (estimator.py:106-109) are never counted from the
+            // screen: a row whose screened predictions all lie above 0.5 + tau
+            // has none, any other row is re-counted in fp64 by k_resolve
+            if (live && !(miny > 0.5f + a.tau)) push_row(a, pl, member);
 
             // ---- per (pair, budget): queue it (k_resolve), or re-evaluate the
             //      winner in fp64 and, fused, decide + scatter it right here ----
