@@ -6,8 +6,8 @@
  * matcher.min_weight_perfect_matching (matcher.py:78-88).
  * rank 1: the Python solver is O(n^3) interpreted (63 s at n = 512).
  *
- * The solver is the O(n^3) primal-dual blossom algorithm on a dense complete
- * graph, run in EXACT integer arithmetic: every weight is a finite double,
+ * The solver is the primal-dual blossom algorithm (O(n^3) on a dense graph),
+ * run on a sparse candidate graph in EXACT integer arithmetic: every weight is a finite double,
  * scaled by a power of two into a 128-bit integer, so tightness tests are
  * exact and the result is a true optimum of the given doubles.
  */
@@ -36,24 +36,30 @@ int cm_max_weight_matching(const double *w, int32_t n, int32_t *mate_out);
  * above, -3 if the matching came out imperfect (internal error). */
 int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out);
 
-/* The same with an explicit candidate degree: the blossom solver runs on the
- * graph of each vertex's k lightest edges, then its LP dual is checked on ALL
- * n(n-1)/2 edges (reduced cost >= 0, the reference's verify-optimum test);
- * violating edges join the candidate set and the solve repeats, so the result
- * is an optimum of the complete graph.  k <= 0 or k >= n - 1: the complete
- * graph directly.  cm_min_weight_perfect_matching uses k = 24. */
+/* The same with an explicit candidate degree k.  Solved as a maximum-weight
+ * PERFECT matching of the reflected values, warm-started and certified:
+ *   - an eps-scaling auction on the assignment relaxation (row-parallel host
+ *     threads) prices every vertex; from those prices the solver derives
+ *     EXACT integer vertex duals feasible on all n(n-1)/2 edges;
+ *   - the blossom solver runs on each vertex's k least-slack edges (plus a
+ *     backbone that guarantees a perfect matching), starting from those duals
+ *     and the tight pairs they imply;
+ *   - its LP dual is checked on ALL n(n-1)/2 edges (reduced cost >= 0, the
+ *     reference's verify-optimum test); violating edges join the candidate set
+ *     and the solve resumes from the previous duals and matching,
+ * so the result is an optimum of the complete graph.  k <= 0 or k >= n - 1:
+ * the complete graph directly.  cm_min_weight_perfect_matching uses k = 24. */
 int cm_min_weight_perfect_matching_k(const double *w, int32_t n, int32_t k, int32_t *mate_out);
 
 /* Minimum-weight perfect matching given vertex potentials with
  * w[u][v] <= pot[u] + pot[v] for every pair -- the pair graph of the sweep
  * has them: a pair's weight is min(co-run, solo_u + solo_v), so pot = the
  * per-app solo times.  Every perfect matching pays sum(pot) minus its
- * "benefit" pot[u] + pot[v] - w[u][v] >= 0, so the optimum is a MAXIMUM-weight
- * matching of the benefit graph (only positive edges: pairs that co-run
- * profitably), certified as above, with the leftover vertices paired in index
- * order (zero benefit between them).  This removes the massive degeneracy of
- * time-share pairs (all perfect matchings of them weigh the same), which makes
- * the direct solve slow.  Returns -4 if `pot` is not a bound. */
+ * "benefit" pot[u] + pot[v] - w[u][v] >= 0, so the optimum is a maximum-weight
+ * PERFECT matching of the benefit graph (zero-benefit edges are the pairs that
+ * time-share), solved and certified as above.  The benefit form keeps the
+ * values small and the auction prices sharp; at n = 4,096 the solve takes
+ * ~2 s on 8 host threads.  Returns -4 if `pot` is not a bound. */
 int cm_min_weight_perfect_matching_pot(const double *w, int32_t n, const double *pot, int32_t k,
                                        int32_t *mate_out);
 

@@ -12,13 +12,18 @@
 // edges carry their scaled integer weights.
 //
 // Minimum-weight perfect matching of the complete graph (cm_min_weight_perfect_
-// matching) is solved on a SPARSE candidate graph -- the k lightest edges of
-// every vertex -- and then certified on the complete graph with the LP dual the
-// solver ends with: every edge's reduced cost y_i + y_j + sum of the duals of
-// the blossoms containing both ends - w_ij must be >= 0 (the reference's
-// verify-optimum condition).  Violating edges are added and the sparse problem
-// re-solved, so the result is a certified optimum of the full graph; the work
-// is ~n^2 k instead of n^3 (seconds instead of hours at n = 4,096).
+// matching*) is solved as a maximum-weight PERFECT matching (certified_perfect):
+// an eps-scaling auction on the assignment relaxation prices the vertices
+// (row-parallel, a persistent host thread pool), the prices give exact integer
+// duals feasible on every edge, the blossom solver runs warm from those duals
+// on a SPARSE candidate graph -- the k least-slack edges of every vertex -- and
+// its LP dual is then certified on the complete graph: every edge's reduced
+// cost y_i + y_j + sum of the duals of the blossoms containing both ends - w_ij
+// must be >= 0 (the reference's verify-optimum condition).  Violating edges
+// are added and the solve resumes from the previous duals and matching, so the
+// result is a certified optimum of the full graph (~2 s at n = 4,096 instead
+// of hours).  The dense O(n^2) scans run in double and re-check near-ties in
+// i128, so every feasibility and tightness fact is exact.
 #include "cosched_match.h"
 
 #include <algorithm>
@@ -26,6 +31,11 @@
 #include <cstdint>
 #include <cstring>
 #include <vector>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 
 namespace {
 
@@ -68,12 +78,23 @@ public:
         allow_.assign((size_t)n * n, 0);
     }
 
+    // Warm start (perfect-matching mode only): vertex duals in the solver's
+    // doubled units at scale `extra`, and a matching whose edges are tight
+    // under them; no blossoms.  Every edge of the graph must have slack >= 0.
+    void warm(const std::vector<i128> &dual, const std::vector<int> &mate, int extra) {
+        extra_ = extra;
+        for (int v = 0; v < n_; ++v) { dual_[v] = dual[v]; mate_[v] = mate[v]; }
+        warm_ = true;
+    }
+
     int run(bool max_cardinality) {
         const int n = n_;
-        // initial duals: doubled vertex duals = max weight (the reference init)
-        i128 maxw = 0;
-        for (const i128 &x : g_.w) maxw = std::max(maxw, x << extra_);
-        for (int v = 0; v < n; ++v) dual_[v] = maxw;
+        if (!warm_) {
+            // initial duals: doubled vertex duals = max weight (the reference init)
+            i128 maxw = 0;
+            for (const i128 &x : g_.w) maxw = std::max(maxw, x << extra_);
+            for (int v = 0; v < n; ++v) dual_[v] = maxw;
+        }
 
         for (int stage = 0; stage < n; ++stage) {
             std::fill(label_.begin(), label_.end(), 0);
@@ -471,6 +492,7 @@ private:
     int n_;
     const Graph &g_;
     int extra_ = 1;        // weights carry one extra factor 2 from the start
+    bool warm_ = false;
     std::vector<int> mate_, label_, inblossom_, parent_, base_, unused_, queue_;
     std::vector<Edge> labeledge_, bestedge_;
     std::vector<std::vector<int>> childs_;
@@ -505,9 +527,19 @@ struct EdgeValue {
 
 // power-of-two shift that turns every edge value into an exact integer
 // (-2 when they span too many binary orders of magnitude for 128 bits)
-int choose_shift(const EdgeValue &f, int *shift) {
+int shift_of(int emin, int emax, int *shift) {
+    if (emin == INT32_MAX) { *shift = 0; return 0; }
+    const int s = 53 - emin;            // ulp(r) = 2^(e-53) -> integer after << s
+    if (emax + s > 96) return -2;       // keep 2^31 of headroom below 2^127 for duals
+    *shift = s;
+    return 0;
+}
+
+// exponent range of the existing nonzero values of rows [u0, u1); -1 if a
+// value is not finite
+int exp_range(const EdgeValue &f, int u0, int u1, int *emin_out, int *emax_out) {
     int emin = INT32_MAX, emax = INT32_MIN;
-    for (int u = 0; u < f.n; ++u)
+    for (int u = u0; u < u1; ++u)
         for (int v = 0; v < f.n; ++v) {
             if (u == v) continue;
             const double r = f(u, v);
@@ -518,11 +550,15 @@ int choose_shift(const EdgeValue &f, int *shift) {
             emin = std::min(emin, e);
             emax = std::max(emax, e);
         }
-    if (emin == INT32_MAX) { *shift = 0; return 0; }
-    const int s = 53 - emin;            // ulp(r) = 2^(e-53) -> integer after << s
-    if (emax + s > 96) return -2;       // keep 2^31 of headroom below 2^127 for duals
-    *shift = s;
+    *emin_out = emin;
+    *emax_out = emax;
     return 0;
+}
+
+int choose_shift(const EdgeValue &f, int *shift) {
+    int emin, emax;
+    if (exp_range(f, 0, f.n, &emin, &emax)) return -1;
+    return shift_of(emin, emax, shift);
 }
 
 inline i128 scaled(double x, int shift) { return (i128)std::ldexp(x, shift); }
@@ -625,8 +661,388 @@ int certified_matching(const EdgeValue &f, int k, int shift, int32_t *mate_out) 
     return -3;
 }
 
-int check_square(const double *w, int32_t n) {
+// Persistent host worker pool for the row-parallel loops of the certified
+// solver (the auction runs thousands of short parallel rounds, so threads are
+// started once per solve, not per loop).
+class RowPool {
+public:
+    RowPool() {
+        int nt = (int)std::thread::hardware_concurrency();
+        nt_ = std::max(1, std::min(nt, 64));
+        for (int t = 1; t < nt_; ++t) th_.emplace_back([this, t] { worker(t); });
+    }
+    ~RowPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto &t : th_) t.join();
+    }
+    int threads() const { return nt_; }
+    // body(i, thread) for i in [0, n); small loops run inline
+    template <class F>
+    void run(int n, F &&body, int grain = 16) {
+        if (nt_ == 1 || n < 2 * grain) {
+            for (int i = 0; i < n; ++i) body(i, 0);
+            return;
+        }
+        std::function<void(int, int)> fn = body;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job_ = &fn;
+            n_ = n;
+            grain_ = grain;
+            next_.store(0);
+            pending_ = nt_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        chew(0);
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [this] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    void chew(int t) {
+        for (;;) {
+            const int i0 = next_.fetch_add(grain_);
+            if (i0 >= n_) break;
+            const int i1 = std::min(n_, i0 + grain_);
+            for (int i = i0; i < i1; ++i) (*job_)(i, t);
+        }
+    }
+    void worker(int t) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            chew(t);
+            std::lock_guard<std::mutex> g(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    int nt_ = 1;
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    std::function<void(int, int)> *job_ = nullptr;
+    int n_ = 0, grain_ = 16, pending_ = 0;
+    std::atomic<int> next_{0};
+};
+
+// Prices of an eps-optimal maximum-weight ASSIGNMENT of the complete graph
+// read as bipartite (row u takes object v != u at value f(u, v)): the
+// fractional relaxation of perfect matching.  Forward auction with
+// eps-scaling, Jacobi rounds (every unassigned row bids in parallel, the
+// highest bid per object wins).  The perfect-matching values are
+// f(u, v) = c_u + d_v - w[u][v] (BENEFIT: c = d = pot; REFLECT: c = r, d = 0),
+// so a row's best object minimizes w[u][v] + (price_v - d_v).  Only the
+// prices are used, and only as guidance: feasibility is restored exactly
+// from them (see certified_perfect).
+std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, RowPool &pool) {
+    const int n = f.n;
+    std::vector<double> price(n, 0.0), h(n, 0.0), d(n, 0.0), c(n, 0.0);
+    for (int v = 0; v < n; ++v) {
+        d[v] = f.kind == EdgeValue::BENEFIT ? f.pot[v] : 0.0;
+        c[v] = f.kind == EdgeValue::BENEFIT ? f.pot[v] : f.reflect;
+    }
+    double vmax = 0.0;
+    {
+        std::vector<double> rmax(n, 0.0);
+        pool.run(n, [&](int u, int) {
+            const double *wr = f.w + (size_t)u * n;
+            double m = INFINITY;
+            for (int v = 0; v < n; ++v) {
+                const double x = v == u ? INFINITY : wr[v] - d[v];
+                m = std::min(m, x);
+            }
+            rmax[u] = c[u] - m;
+        });
+        for (double x : rmax) vmax = std::max(vmax, x);
+    }
+    if (!(vmax > 0.0)) return price;
+    std::vector<int> owner(n), bid_obj(n), freerows, next, best(n, -1);
+    std::vector<double> bid_val(n);
+    freerows.reserve(n);
+    next.reserve(n);
+    for (double eps = vmax / 8;; eps /= 6) {
+        std::fill(owner.begin(), owner.end(), -1);
+        freerows.resize(n);
+        for (int u = 0; u < n; ++u) freerows[u] = u;
+        for (int it = 0; !freerows.empty() && it < 1000000; ++it) {
+            for (int v = 0; v < n; ++v) h[v] = price[v] - d[v];
+            const int nf = (int)freerows.size();
+            pool.run(nf, [&](int q, int) {
+                const int u = freerows[q];
+                const double *wr = f.w + (size_t)u * n;
+                double m1 = INFINITY, m2 = INFINITY;   // two smallest w + h, v != u
+                int j1 = -1;
+                auto scan = [&](int v0, int v1) {
+                    for (int v = v0; v < v1; ++v) {
+                        const double x = wr[v] + h[v];
+                        if (x < m2) {
+                            if (x < m1) { m2 = m1; m1 = x; j1 = v; }
+                            else m2 = x;
+                        }
+                    }
+                };
+                scan(0, u);
+                scan(u + 1, n);
+                if (m2 == INFINITY) m2 = m1;
+                bid_obj[q] = j1;
+                bid_val[q] = price[j1] + (m2 - m1) + eps;
+            }, 4);
+            next.clear();
+            for (int q = 0; q < nf; ++q) {
+                const int v = bid_obj[q];
+                if (best[v] < 0 || bid_val[q] > bid_val[best[v]]) best[v] = q;
+            }
+            for (int q = 0; q < nf; ++q) {
+                const int v = bid_obj[q], u = freerows[q];
+                if (best[v] != q) { next.push_back(u); continue; }
+                if (owner[v] >= 0) next.push_back(owner[v]);
+                owner[v] = u;
+                price[v] = bid_val[q];
+            }
+            for (int q = 0; q < nf; ++q) best[bid_obj[q]] = -1;
+            freerows.swap(next);
+        }
+        if (eps <= eps_final_rel * vmax) break;
+    }
+    return price;
+}
+
+// Maximum-weight PERFECT matching of the complete graph (every u != v is an
+// edge of value f(u, v) >= 0), warm-started and certified:
+//   1. guidance: prices p of the assignment relaxation (auction_prices);
+//   2. exact, globally feasible start: with P = p scaled to the solver's
+//      integers, a_u = max_v (2 f(u, v) - P_v) and y_u = a_u + P_u every
+//      slack y_u + y_v - 2 f(u, v) = (a_u + P_v - 2f) + (a_v + P_u - 2f) is
+//      >= 0 on ALL n(n-1)/2 edges; good prices make the optimal pairs nearly
+//      tight, so they rank first by slack;
+//   3. candidates: the k least-slack edges of every vertex (row-parallel);
+//      jump start: in vertex order each free v lowers y_v to its tightest
+//      edge over the complete graph (all slacks stay >= 0) and takes that
+//      partner if it is free; plus a backbone (greedy matching of the
+//      candidates, leftovers paired in order) so a perfect matching exists;
+//   4. the blossom solver in max-cardinality mode from that matching and
+//      those duals (for the perfect-matching LP the vertex duals are free);
+//   5. the LP dual certificate on every edge of the complete graph
+//      (row-parallel).  Violating edges join the candidates; the duals are
+//      flattened (each blossom dual added to its vertices, which keeps every
+//      slack >= 0), each row's violators made tight by one raise of that row's
+//      vertex, matched edges that lost tightness unmatched, and step 4 resumes.
+// The result is an optimum of the complete graph (the final certificate is
+// the reference's verify-optimum condition on all n(n-1)/2 edges).
+int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, RowPool &pool) {
+    const int n = f.n;
+    if (k <= 0 || k >= n - 1) k = n - 1;
+    int extra = 1;
+    auto W = [&](int u, int v) { return scaled(f(u, v), shift) << extra; };
+    // Every exact integer below has a double shadow: Wd = f * 2^(shift+extra)
+    // is the exact weight as a double (a power-of-two scaling), so sums of a
+    // few such terms are off by a few ulps of their magnitude.  The dense
+    // O(n^2) scans run in double and re-check in i128 only the entries within
+    // `tol` of the decision, so every feasibility / tightness fact is exact.
+    auto Wd = [&](int u, int v) { return std::ldexp(f(u, v), shift + extra); };
+    double mag = 0.0;
+    for (int u = 0; u < n; ++u) mag = std::max(mag, std::fabs(Wd(u, u == 0 ? 1 : 0)));
+    // ---- 1-2. prices -> exact feasible duals ----
+    std::vector<i128> dual(n, 0), P(n, 0);
+    std::vector<double> dd(n, 0.0);
+    double tol = 0.0;
+    {
+        const std::vector<double> price = auction_prices(f, 3e-3, pool);
+        std::vector<double> Pd(n);
+        for (int v = 0; v < n; ++v) {
+            P[v] = 2 * (scaled(price[v], shift) << extra);
+            Pd[v] = (double)P[v];
+            mag = std::max(mag, std::fabs(Pd[v]));
+        }
+        std::vector<double> rowmax(n, 0.0);
+        pool.run(n, [&](int u, int) {
+            double m = 0.0;
+            for (int v = 0; v < n; ++v)
+                if (v != u) m = std::max(m, std::fabs(Wd(u, v)));
+            rowmax[u] = m;
+        });
+        for (double x : rowmax) mag = std::max(mag, x);
+        tol = std::ldexp(mag, -40);       // >> the rounding of any 8-term sum
+        pool.run(n, [&](int u, int) {
+            double best = -INFINITY;
+            for (int v = 0; v < n; ++v)
+                if (v != u) best = std::max(best, 2 * Wd(u, v) - Pd[v]);
+            i128 a = 0;
+            bool any = false;
+            for (int v = 0; v < n; ++v) {
+                if (v == u || 2 * Wd(u, v) - Pd[v] < best - 8 * tol) continue;
+                const i128 x = 2 * W(u, v) - P[v];
+                if (!any || x > a) { a = x; any = true; }
+            }
+            dual[u] = (a + P[u]) / 2;      // a + P even: both terms are even
+            dd[u] = (double)dual[u];
+        });
+    }
+    // ---- 3. candidates by slack (double: a heuristic), jump start, backbone ----
+    std::vector<std::vector<int>> cand(n);
+    pool.run(n, [&](int u, int) {
+        std::vector<std::pair<double, int>> row;
+        row.reserve(n);
+        for (int v = 0; v < n; ++v)
+            if (v != u) row.push_back({dd[u] + dd[v] - 2 * Wd(u, v), v});
+        std::partial_sort(row.begin(), row.begin() + k, row.end());
+        for (int q = 0; q < k; ++q) cand[u].push_back(row[q].second);
+    });
+    std::vector<std::pair<int, int>> edges;
     for (int u = 0; u < n; ++u)
+        for (int v : cand[u]) edges.push_back({std::min(u, v), std::max(u, v)});
+    std::vector<int> mate(n, -1);
+    {
+        std::vector<double> need(n);
+        for (int v = 0; v < n; ++v) {
+            if (mate[v] >= 0) continue;
+            // exact max_u (2 W_uv - y_u): double scan, i128 on the near-max
+            double bd = -INFINITY;
+            for (int u = 0; u < n; ++u) {
+                need[u] = u == v ? -INFINITY : 2 * Wd(u, v) - dd[u];
+                bd = std::max(bd, need[u]);
+            }
+            i128 best = 0;
+            int arg = -1;
+            bool arg_free = false;
+            for (int u = 0; u < n; ++u) {
+                if (u == v || need[u] < bd - 8 * tol) continue;
+                const i128 x = 2 * W(u, v) - dual[u];
+                const bool fr = mate[u] < 0;
+                if (arg < 0 || x > best || (x == best && fr && !arg_free)) {
+                    best = x; arg = u; arg_free = fr;
+                }
+            }
+            dual[v] = best;
+            dd[v] = (double)best;
+            if (arg_free) {
+                mate[v] = arg; mate[arg] = v;
+                edges.push_back({std::min(v, arg), std::max(v, arg)});
+            }
+        }
+    }
+    std::sort(edges.begin(), edges.end());
+    edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+    {
+        std::vector<std::pair<double, int>> order(edges.size());
+        for (size_t q = 0; q < edges.size(); ++q) {
+            const int u = edges[q].first, v = edges[q].second;
+            order[q] = {dd[u] + dd[v] - 2 * Wd(u, v), (int)q};
+        }
+        std::sort(order.begin(), order.end());
+        std::vector<char> used(n, 0);
+        for (auto &o : order) {
+            const int u = edges[o.second].first, v = edges[o.second].second;
+            if (!used[u] && !used[v]) used[u] = used[v] = 1;
+        }
+        int prev = -1;
+        for (int v = 0; v < n; ++v) {
+            if (used[v]) continue;
+            if (prev < 0) { prev = v; continue; }
+            edges.push_back({prev, v});
+            prev = -1;
+        }
+        std::sort(edges.begin(), edges.end());
+        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+    }
+    Graph g = make_graph(f, edges, shift);
+    int extra0 = extra;
+
+    for (int round = 0; round < 64; ++round) {
+        Blossom m(g);
+        m.warm(dual, mate, extra);
+        m.run(true);
+        extra = m.extra();
+        const std::vector<i128> &bd = m.duals();
+        const std::vector<int> &parent = m.parents();
+        const std::vector<int> &mm = m.mate();
+        std::vector<std::vector<int>> chain(n);   // enclosing blossoms, outermost first
+        for (int v = 0; v < n; ++v) {
+            for (int b = parent[v]; b >= 0; b = parent[b]) chain[v].push_back(b);
+            std::reverse(chain[v].begin(), chain[v].end());
+        }
+        if (extra != extra0) {             // the solver doubled its scale
+            for (int q = 0; q < extra - extra0; ++q) tol *= 2;
+            extra0 = extra;
+        }
+        std::vector<double> fd(n);
+        for (int v = 0; v < n; ++v) fd[v] = (double)bd[v];
+        // certificate on the complete graph (every edge of a single vertex too)
+        std::vector<std::vector<std::pair<i128, int>>> bad(n);
+        pool.run(n, [&](int i, int) {
+            std::vector<std::pair<i128, int>> worst;
+            for (int j = 0; j < n; ++j) {
+                if (j == i) continue;
+                if (mm[i] < 0) { worst.push_back({0, j}); continue; }   // every edge of a single
+                if (mm[j] < 0) continue;                                  // (added by j's row)
+                const auto &ci = chain[i], &cj = chain[j];
+                if (ci.empty() || cj.empty() || ci[0] != cj[0]) {
+                    // no common blossom: the double reduced cost decides
+                    // unless it is within tol of 0
+                    if (fd[i] + fd[j] - 2 * Wd(i, j) > 8 * tol) continue;
+                }
+                i128 z = 0;
+                for (size_t q = 0; q < ci.size() && q < cj.size() && ci[q] == cj[q]; ++q) z += bd[ci[q]];
+                const i128 red = bd[i] + bd[j] + 2 * z - 2 * W(i, j);
+                if (red < 0) worst.push_back({red, j});
+            }
+            const size_t cap = 8;
+            if (mm[i] >= 0 && worst.size() > cap) {
+                std::partial_sort(worst.begin(), worst.begin() + cap, worst.end());
+                worst.resize(cap);
+            }
+            bad[i] = std::move(worst);
+        });
+        size_t nbad = 0;
+        for (int i = 0; i < n; ++i) nbad += bad[i].size();
+        if (nbad == 0) {
+            for (int v = 0; v < n; ++v) mate_out[v] = mm[v];
+            return 0;
+        }
+        for (int i = 0; i < n; ++i)
+            for (auto &x : bad[i]) edges.push_back({std::min(i, x.second), std::max(i, x.second)});
+        std::sort(edges.begin(), edges.end());
+        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+        g = make_graph(f, edges, shift);
+        // warm state for the next round: flattened duals, violators made tight
+        for (int v = 0; v < n; ++v) {
+            i128 y = bd[v];
+            for (int b = parent[v]; b >= 0; b = parent[b]) y += bd[b];
+            dual[v] = y;
+        }
+        mate.assign(mm.begin(), mm.end());
+        for (int i = 0; i < n; ++i) {
+            i128 deficit = 0;
+            for (auto &x : bad[i]) {
+                const i128 red = dual[i] + dual[x.second] - 2 * W(i, x.second);
+                if (red < 0 && -red > deficit) deficit = -red;
+            }
+            dual[i] += deficit;
+        }
+        for (int v = 0; v < n; ++v) {
+            const int u = mate[v];
+            if (u > v && dual[u] + dual[v] != 2 * W(u, v)) { mate[u] = -1; mate[v] = -1; }
+        }
+    }
+    return -3;
+}
+
+int check_rows(const double *w, int32_t n, int u0, int u1) {
+    for (int u = u0; u < u1; ++u)
         for (int v = 0; v < n; ++v) {
             const double x = w[(size_t)u * n + v];
             if (!std::isfinite(x)) return -1;
@@ -635,11 +1051,43 @@ int check_square(const double *w, int32_t n) {
     return 0;
 }
 
+int check_square(const double *w, int32_t n) { return check_rows(w, n, 0, n); }
+
+// The O(n^2) input checks and scale choice of the perfect-matching entry
+// points, row-parallel: symmetric finite w, optional potential bound
+// (-4 if violated), exponent range -> shift.
+int prepare_parallel(const EdgeValue &f, const double *pot, RowPool &pool, int *shift) {
+    const int n = f.n;
+    const int nt = pool.threads();
+    std::vector<int> bad(nt, 0), lo(nt, INT32_MAX), hi(nt, INT32_MIN);
+    pool.run(n, [&](int u, int t) {
+        if (check_rows(f.w, n, u, u + 1)) { bad[t] = -1; return; }
+        if (pot) {
+            if (!std::isfinite(pot[u])) { bad[t] = -1; return; }
+            for (int v = 0; v < n; ++v)
+                if (u != v && f.w[(size_t)u * n + v] > pot[u] + pot[v]) { if (!bad[t]) bad[t] = -4; return; }
+        }
+        int e0, e1;
+        if (exp_range(f, u, u + 1, &e0, &e1)) { bad[t] = -1; return; }
+        lo[t] = std::min(lo[t], e0);
+        hi[t] = std::max(hi[t], e1);
+    });
+    for (int t = 0; t < nt; ++t)
+        if (bad[t] == -1) return -1;
+    for (int t = 0; t < nt; ++t)
+        if (bad[t]) return bad[t];
+    int emin = INT32_MAX, emax = INT32_MIN;
+    for (int t = 0; t < nt; ++t) { emin = std::min(emin, lo[t]); emax = std::max(emax, hi[t]); }
+    return shift_of(emin, emax, shift);
+}
+
 }  // namespace
 
 extern "C" {
 
-const char *cm_version(void) { return "cosched_match 0.3.0 (exact int128 blossom, sparse + dual certificate)"; }
+const char *cm_version(void) {
+    return "cosched_match 0.4.0 (exact int128 blossom, auction-priced warm start, sparse + dual certificate)";
+}
 
 int cm_max_weight_matching(const double *w, int32_t n, int32_t *mate_out) {
     if (n < 0 || (n > 0 && (!w || !mate_out))) return -1;
@@ -658,14 +1106,20 @@ int cm_min_weight_perfect_matching(const double *w, int32_t n, int32_t *mate_out
 
 int cm_min_weight_perfect_matching_k(const double *w, int32_t n, int32_t k, int32_t *mate_out) {
     if (n < 2 || (n & 1) || !w || !mate_out) return -1;
-    if (check_square(w, n)) return -1;
+    RowPool pool;
+    std::vector<double> rmx(n, -INFINITY);
+    pool.run(n, [&](int u, int) {
+        double m = -INFINITY;
+        for (int v = 0; v < n; ++v) m = std::max(m, w[(size_t)u * n + v]);
+        rmx[u] = m;
+    });
     double mx = -INFINITY;
-    for (size_t q = 0; q < (size_t)n * n; ++q) mx = std::max(mx, w[q]);
+    for (double x : rmx) mx = std::max(mx, x);
     EdgeValue f{EdgeValue::REFLECT, w, n, mx + 1.0, nullptr};   // matcher.py:84
     int shift = 0;
-    int rc = choose_shift(f, &shift);
+    int rc = prepare_parallel(f, nullptr, pool, &shift);
     if (rc) return rc;
-    rc = certified_matching(f, k, shift, mate_out);
+    rc = certified_perfect(f, k, shift, mate_out, pool);
     if (rc) return rc;
     for (int v = 0; v < n; ++v)
         if (mate_out[v] < 0) return -3;
@@ -675,29 +1129,16 @@ int cm_min_weight_perfect_matching_k(const double *w, int32_t n, int32_t k, int3
 int cm_min_weight_perfect_matching_pot(const double *w, int32_t n, const double *pot, int32_t k,
                                        int32_t *mate_out) {
     if (n < 2 || (n & 1) || !w || !pot || !mate_out) return -1;
-    if (check_square(w, n)) return -1;
-    for (int u = 0; u < n; ++u) {
-        if (!std::isfinite(pot[u])) return -1;
-        for (int v = 0; v < n; ++v)
-            if (u != v && w[(size_t)u * n + v] > pot[u] + pot[v]) return -4;   // not a potential bound
-    }
+    RowPool pool;
     EdgeValue f{EdgeValue::BENEFIT, w, n, 0.0, pot};
     int shift = 0;
-    int rc = choose_shift(f, &shift);
+    int rc = prepare_parallel(f, pot, pool, &shift);
     if (rc) return rc;
-    rc = certified_matching(f, k, shift, mate_out);
+    rc = certified_perfect(f, k, shift, mate_out, pool);
     if (rc) return rc;
-    // vertices left single pair up in index order: between two of them the
-    // benefit is 0, so any pairing completes an optimal perfect matching
-    int prev = -1;
-    for (int v = 0; v < n; ++v) {
-        if (mate_out[v] >= 0) continue;
-        if (prev < 0) { prev = v; continue; }
-        mate_out[prev] = v;
-        mate_out[v] = prev;
-        prev = -1;
-    }
-    return prev < 0 ? 0 : -3;
+    for (int v = 0; v < n; ++v)
+        if (mate_out[v] < 0) return -3;
+    return 0;
 }
 
 }  // extern "C"

@@ -102,7 +102,7 @@ def min_weight_perfect_matching(graph: PairGraph) -> list:
     rc = None
     if pot_fn is not None:
         pot = pot_fn()
-        k = 64 if n <= 256 else 24
+        k = 48
         rc = lib.cm_min_weight_perfect_matching_pot(nat.ptr(w), n, nat.ptr(pot), k,
                                                     nat.ptr(mate, nat.c_int32_p))
     if rc is None or rc == -4:

@@ -149,3 +149,54 @@ def test_potential_form_equals_direct_on_sweep_graphs():
         mate = np.empty(n, dtype=np.int32)
         assert nat.match_lib().cm_min_weight_perfect_matching_pot(
             nat.ptr(W), n, nat.ptr(bad), 8, nat.ptr(mate, nat.c_int32_p)) == -4
+
+
+def _mate_weight(W, mate):
+    n = len(mate)
+    assert sorted(int(x) for x in mate) == list(range(n))
+    assert all(mate[int(mate[v])] == v and mate[v] != v for v in range(n))
+    return sum(W[v, int(mate[v])] for v in range(n) if v < mate[v])
+
+
+def test_warm_started_solver_on_a_512_app_sweep_graph():
+    """The auction-priced, warm-started certified solver (benefit and reflected
+    forms, two candidate degrees) reaches the dense solve's optimum on a real
+    512-app pair graph (oracle sweep) -- the size where several certificate
+    rounds and blossoms actually occur."""
+    import oracle
+    from conftest import workload
+    from paper_2405_03831_b200 import _native as nat, core, fnn
+    from paper_2405_03831_b200.grid import KnobGrid
+    w = fnn.load_weights(os.path.join(GOLDEN, "weights.json"))
+    n = 512
+    F, T = workload(n, 5)
+    r = oracle.sweep(w, F, T, KnobGrid([core.default_space(400.0)]))
+    W = np.zeros((n, n))
+    iu, ju = np.triu_indices(n, 1)
+    W[iu, ju] = r["weight"][0]
+    W = np.ascontiguousarray(W + W.T)
+    pot = np.ascontiguousarray(r["solo_time"][0])
+    lib = nat.match_lib()
+    out = []
+    for call in (lambda m: lib.cm_min_weight_perfect_matching_pot(nat.ptr(W), n, nat.ptr(pot), 48, nat.ptr(m, nat.c_int32_p)),
+                 lambda m: lib.cm_min_weight_perfect_matching_pot(nat.ptr(W), n, nat.ptr(pot), 4, nat.ptr(m, nat.c_int32_p)),
+                 lambda m: lib.cm_min_weight_perfect_matching_k(nat.ptr(W), n, 8, nat.ptr(m, nat.c_int32_p)),
+                 lambda m: lib.cm_min_weight_perfect_matching_k(nat.ptr(W), n, 0, nat.ptr(m, nat.c_int32_p))):
+        mate = np.empty(n, dtype=np.int32)
+        assert call(mate) == 0
+        out.append(_mate_weight(W, mate))
+    assert max(out) - min(out) <= 1e-12 * min(out)
+
+
+def test_all_time_share_graph_is_fully_degenerate_but_solved():
+    """Every pair time-shares (w = pot_i + pot_j: zero benefit everywhere), so
+    every perfect matching is optimal -- the solver must still return one."""
+    from paper_2405_03831_b200 import _native as nat
+    n = 64
+    pot = np.ascontiguousarray(np.random.default_rng(3).uniform(1.0, 9.0, n))
+    W = np.ascontiguousarray(pot[:, None] + pot[None, :])
+    np.fill_diagonal(W, 0.0)
+    mate = np.empty(n, dtype=np.int32)
+    assert nat.match_lib().cm_min_weight_perfect_matching_pot(
+        nat.ptr(W), n, nat.ptr(pot), 8, nat.ptr(mate, nat.c_int32_p)) == 0
+    assert abs(_mate_weight(W, mate) - pot.sum()) <= 1e-12 * pot.sum()
