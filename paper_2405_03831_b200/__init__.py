@@ -14,15 +14,16 @@ __version__ = "0.1.0"
 from .core import (ConfigSpace, HardwareConfig, JobProfile, JobSet, Schedule,
                    SchedulingParams, ValidationError, default_space, enumerate_corun_configs,
                    enumerate_solo_splits, normalize_input, solo_config)
-from .fnn import NetworkWeights, forward, forward_batch, initialize_weights, load_weights, save_weights
+from .fnn import (LabeledSample, NetworkWeights, TrainingConfig, TrainingDivergedError, backward,
+                  forward, forward_batch, initialize_weights, load_weights, save_weights, train)
 from .estimator import (FnnSlowdownModel, SlowdownQuery, as_model, clamp_stats, corun_app_time,
                         corun_time, slowdown, solo_app_time, solorun_time)
 from .hwopt import PairDecision, decide_pair, optimize_corun, optimize_solo_pair
 from .matcher import PairGraph, brute_force_matching, matching_weight, min_weight_perfect_matching
 from .scheduler import (SchedulerInput, build_graph, predicted_makespan, schedule,
                         schedule_to_json, set_time)
-from .simenv import (OracleParams, OracleSlowdownModel, SyntheticJobSpec, generate_workload,
-                     mixed_archetypes, oracle_slowdown)
+from .simenv import (OracleParams, OracleSlowdownModel, SyntheticJobSpec, generate_dataset,
+                     generate_workload, mixed_archetypes, oracle_slowdown)
 from .grid import KnobGrid
 
 __all__ = [name for name in dir() if not name.startswith("_")]
@@ -33,6 +34,9 @@ def __getattr__(name):
     if name in ("sweep_pairs", "SweepResult", "plan_for"):
         from . import sweep
         return getattr(sweep, name)
+    if name == "train_many":
+        from .trainer import train_many
+        return train_many
     if name == "SweepPlan":
         from .device import SweepPlan
         return SweepPlan

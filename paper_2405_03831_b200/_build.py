@@ -2,6 +2,8 @@
 
 * ``libcosched_b200.so``: ``nvcc -gencode arch=compute_100a,code=sm_100a`` of
   ``csrc/sweep.cu``, static cudart, so the .so only needs the driver.
+* ``libcosched_train.so``: ``nvcc`` (same flags) of ``csrc/train.cu``, the
+  device-side trainer (include/cosched_train.h).
 * ``libcosched_match.so``: ``g++`` of ``csrc/matching.cpp`` (host only).
 
 Outputs sit next to the package sources (git-ignored, shipped to the GPU box
@@ -22,7 +24,7 @@ CSRC = os.path.join(HERE, "csrc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
                      "-cudart", "static", f"-I{INCLUDE}"]
-CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{INCLUDE}"]
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra", f"-I{INCLUDE}"]
 
 
 def _nvcc() -> str:
@@ -66,8 +68,17 @@ def build_matcher(force: bool = False, verbose: bool = True) -> str:
     return out
 
 
+def build_train(force: bool = False, verbose: bool = True) -> str:
+    out = os.path.join(HERE, "libcosched_train.so")
+    src = os.path.join(CSRC, "train.cu")
+    deps = [src, os.path.join(INCLUDE, "cosched_train.h")]
+    if force or _stale(out, deps):
+        _run([_nvcc(), *NVCC_FLAGS, src, "-o", out], verbose)
+    return out
+
+
 def build_all(force: bool = False, verbose: bool = True) -> list:
-    return [build_sweep(force, verbose), build_matcher(force, verbose)]
+    return [build_sweep(force, verbose), build_train(force, verbose), build_matcher(force, verbose)]
 
 
 if __name__ == "__main__":

@@ -2,9 +2,11 @@
 
 * ``libcosched_b200.so``  -- sm_100a sweep kernels (include/cosched_b200.h),
   built from ``csrc/sweep.cu`` with ``-gencode arch=compute_100a,code=sm_100a``.
+* ``libcosched_train.so`` -- sm_100a device-side trainer (include/cosched_train.h),
+  built from ``csrc/train.cu``.
 * ``libcosched_match.so`` -- host C++ Edmonds matching (include/cosched_match.h).
 
-Both live next to this file (built by ``__graft_entry__.build()``).  There is
+All live next to this file (built by ``__graft_entry__.build()``).  There is
 no fallback: a missing library raises ``NativeLibraryError`` with the build
 command, so a GPU box never silently runs a CPU path.
 """
@@ -18,6 +20,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SWEEP_LIB = os.path.join(_HERE, "libcosched_b200.so")
 MATCH_LIB = os.path.join(_HERE, "libcosched_match.so")
+TRAIN_LIB = os.path.join(_HERE, "libcosched_train.so")
 
 MAX_BUDGETS = 8
 KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT = 0, 1, 2
@@ -158,6 +161,16 @@ SWEEP_SYMBOLS = {
                                            ctypes.c_void_p]),
 }
 
+TRAIN_SYMBOLS = {
+    "ct_version": (ctypes.c_char_p, []),
+    "ct_backward": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ct_train_sgd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                    ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32,
+                                    ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+}
+
 MATCH_SYMBOLS = {
     "cm_version": (ctypes.c_char_p, []),
     "cm_max_weight_matching": (ctypes.c_int, [c_double_p, ctypes.c_int32, c_int32_p]),
@@ -195,6 +208,10 @@ def sweep_lib():
 
 def match_lib():
     return _load(MATCH_LIB, MATCH_SYMBOLS, "C++ matching library")
+
+
+def train_lib():
+    return _load(TRAIN_LIB, TRAIN_SYMBOLS, "CUDA training extension")
 
 
 def check(rc: int, what: str) -> None:

@@ -5,15 +5,25 @@ Mirrors ``cosched.fnn`` (``pkg/src/cosched/fnn.py``) for what the sweep needs:
 (``save_weights``/``load_weights``, fnn.py:311-359), seeded Glorot init
 (fnn.py:122-143) and inference (``forward``/``forward_batch``,
 fnn.py:146-165).  Inference runs on the GPU through the C ABI
-(``cs_forward_rows``), in fp64, with no CPU fallback.  Training (backprop,
-SGD, dataset split; fnn.py:168-308) is out of scope for this build: it is
-offline, ~50 s on a CPU and not on the sweep path.
+(``cs_forward_rows``), in fp64, with no CPU fallback.
+
+Training mirrors fnn.py:23-28, 71-119 and 168-308 (``TrainingConfig``,
+``LabeledSample``, ``Gradients``, ``EpochStats``, ``split_dataset``,
+``epoch_batch_order``, ``sgd_step``, ``backward``, ``train``,
+``write_loss_csv``): the seeded split / permutations / init are the
+reference's numpy draws (host), while every gradient step runs on the GPU --
+``backward`` as one kernel launch, ``train`` as ONE persistent kernel per run
+that walks all epochs and batches with the parameters resident in shared
+memory (``csrc/train.cu``, ``include/cosched_train.h``).  ``train_many``
+trains several seeds concurrently, one SM each.
 """
 
 from __future__ import annotations
 
+import csv
 import json
 from dataclasses import dataclass
+from typing import Sequence
 
 import numpy as np
 
@@ -140,3 +150,155 @@ def forward(weights: NetworkWeights, x) -> float:
     if bad.any():
         raise ValidationError(f"input entry {int(np.argmax(bad))} is not finite")
     return float(forward_batch(weights, x[None, :])[0])
+
+
+# ---------------------------------------------------------------------------
+# training (fnn.py:23-28, 71-119, 168-308)
+# ---------------------------------------------------------------------------
+
+class TrainingDivergedError(RuntimeError):
+    """Raised when the training loss stops being finite (fnn.py:23-28)."""
+
+    def __init__(self, epoch: int):
+        super().__init__(f"training loss became non-finite at epoch {epoch}")
+        self.epoch = epoch
+
+
+@dataclass(frozen=True)
+class TrainingConfig:
+    """SGD hyperparameters; defaults follow the standard recipe (fnn.py:71-89)."""
+
+    learning_rate: float = 0.001
+    batch_size: int = 4
+    epochs: int = 200
+    seed: int = 0
+    validation_fraction: float = 0.2
+
+    def __post_init__(self) -> None:
+        if self.learning_rate <= 0:
+            raise ValidationError("learning_rate must be > 0")
+        if self.batch_size < 1:
+            raise ValidationError("batch_size must be >= 1")
+        if self.epochs < 1:
+            raise ValidationError("epochs must be >= 1")
+        if not 0.0 < self.validation_fraction < 1.0:
+            raise ValidationError("validation_fraction must be in (0, 1)")
+
+
+@dataclass(frozen=True)
+class LabeledSample:
+    """One normalized 40-vector input and its slowdown target (fnn.py:92-107)."""
+
+    input: np.ndarray
+    target: float
+
+    def __post_init__(self) -> None:
+        x = np.asarray(self.input, dtype=float)
+        if x.shape != (INPUT_DIM,):
+            raise ValidationError(f"sample input must have {INPUT_DIM} entries, got {x.shape}")
+        x = x.copy()
+        x.setflags(write=False)
+        object.__setattr__(self, "input", x)
+        if not np.isfinite(self.target):
+            raise ValidationError("sample target must be finite")
+
+
+@dataclass
+class Gradients:
+    """Parameter gradients, congruent with NetworkWeights (fnn.py:110-119)."""
+
+    w1: np.ndarray
+    b1: np.ndarray
+    w2: np.ndarray
+    b2: np.ndarray
+    w_out: np.ndarray
+    b_out: np.ndarray
+
+
+@dataclass(frozen=True)
+class EpochStats:
+    epoch: int
+    train_mse: float
+    val_mse: float
+
+
+_PARAM_SHAPES = (("w1", (HIDDEN_DIM, INPUT_DIM)), ("b1", (HIDDEN_DIM,)),
+                 ("w2", (HIDDEN_DIM, HIDDEN_DIM)), ("b2", (HIDDEN_DIM,)),
+                 ("w_out", (1, HIDDEN_DIM)), ("b_out", (1,)))
+N_PARAMS = sum(int(np.prod(s)) for _, s in _PARAM_SHAPES)     # CT_NPARAM = 1099
+
+
+def flat_params(weights) -> np.ndarray:
+    """The flat fp64 parameter vector of include/cosched_train.h."""
+    return np.concatenate([np.asarray(getattr(weights, k), dtype=np.float64).ravel()
+                           for k, _ in _PARAM_SHAPES])
+
+
+def _split_params(vec: np.ndarray) -> dict:
+    out, i = {}, 0
+    for k, shape in _PARAM_SHAPES:
+        size = int(np.prod(shape))
+        out[k] = np.array(vec[i:i + size]).reshape(shape)
+        i += size
+    return out
+
+
+def weights_from_flat(vec: np.ndarray, feature_bounds) -> NetworkWeights:
+    return NetworkWeights(feature_bounds=feature_bounds, **_split_params(vec))
+
+
+def split_dataset(dataset: Sequence[LabeledSample], cfg: TrainingConfig):
+    """Seeded shuffle split into (train, validation) lists (fnn.py:219-231)."""
+    rng = np.random.default_rng([cfg.seed, 0])
+    order = rng.permutation(len(dataset))
+    n_val = int(len(dataset) * cfg.validation_fraction)
+    return [dataset[i] for i in order[n_val:]], [dataset[i] for i in order[:n_val]]
+
+
+def epoch_batch_order(cfg: TrainingConfig, n_train: int, epoch: int) -> np.ndarray:
+    """The deterministic sample permutation of one epoch (fnn.py:234-237)."""
+    rng = np.random.default_rng([cfg.seed, 1 + epoch])
+    return rng.permutation(n_train)
+
+
+def sgd_step(weights: NetworkWeights, grads: Gradients, lr: float) -> NetworkWeights:
+    """One plain SGD update; fresh weights, inputs untouched (fnn.py:247-257)."""
+    return NetworkWeights(
+        w1=weights.w1 - lr * grads.w1, b1=weights.b1 - lr * grads.b1,
+        w2=weights.w2 - lr * grads.w2, b2=weights.b2 - lr * grads.b2,
+        w_out=weights.w_out - lr * grads.w_out, b_out=weights.b_out - lr * grads.b_out,
+        feature_bounds=weights.feature_bounds)
+
+
+def backward(weights: NetworkWeights, batch: Sequence[LabeledSample]):
+    """Gradients of the batch mean squared error plus the loss (fnn.py:174-210),
+    computed on the GPU (ct_backward).  The ReLU subgradient at 0 is 0."""
+    if len(batch) == 0:
+        raise ValidationError("backward needs a nonempty batch")
+    from .trainer import device_backward
+    g, loss = device_backward(weights, batch)
+    return Gradients(**_split_params(g)), loss
+
+
+def train(dataset: Sequence[LabeledSample], cfg: TrainingConfig, feature_bounds=None):
+    """Mini-batch SGD training, bit-reproducible for a fixed seed (fnn.py:260-297).
+
+    Same split, init and per-epoch permutations as the reference (its numpy
+    draws); the epochs themselves run as one persistent GPU kernel.  The
+    per-epoch train MSE averages the batch losses as seen before each update,
+    the validation MSE is taken after the epoch.
+
+    Raises:
+        TrainingDivergedError: when a batch loss stops being finite.
+    """
+    from .trainer import train_many
+    return train_many(dataset, [cfg], feature_bounds)[0]
+
+
+def write_loss_csv(history: Sequence[EpochStats], path) -> None:
+    """Training log: one row per epoch (fnn.py:362-369)."""
+    with open(path, "w", newline="") as fh:
+        writer = csv.writer(fh)
+        writer.writerow(["epoch", "train_mse", "val_mse"])
+        for row in history:
+            writer.writerow([row.epoch, repr(row.train_mse), repr(row.val_mse)])

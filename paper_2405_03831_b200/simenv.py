@@ -11,8 +11,8 @@ Mirrors the reference's public names (``pkg/src/cosched/simenv.py``):
 * the analytic oracle model -- ``OracleParams``, ``OracleSlowdownModel``,
   ``oracle_slowdown`` (simenv.py:63-237), served by ``analytic.py`` (its
   batched form is the exact GPU sweep ``cs_analytic_sweep``);
-* the training dataset -- ``generate_dataset`` (simenv.py:393-469), in
-  ``dataset.py``.
+* the training dataset -- ``generate_dataset``, ``Dataset``, ``DatasetRow``
+  and the CSV form (simenv.py:330-505), in ``dataset.py``.
 
 The policy harness (``run_policy``, reports) and the CLI stay out of scope
 (SURVEY.md §2).
@@ -27,6 +27,8 @@ from typing import Sequence
 import numpy as np
 
 from .analytic import OracleParams, OracleSlowdownModel, oracle_slowdown  # noqa: F401
+from .dataset import (DATASET_INPUT_COLUMNS, Dataset, DatasetRow, dataset_to_csv,  # noqa: F401
+                      generate_dataset, load_dataset_csv)
 from .core import JobProfile, ValidationError
 from .synth import ARCHETYPE_RANGES, ARCHETYPES, BASE_TIME_RANGE, job_ids, mixed_archetypes  # noqa: F401
 

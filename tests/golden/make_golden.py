@@ -29,6 +29,11 @@ Stages and what they pin (reference file:line):
   (``cosched.core.CPU_CAPS/GPU_CAPS`` monkeypatched, as SURVEY.md §8d says).
 * ``matching``  -- ``matching.json``: reference ``min_weight_perfect_matching``
   and ``brute_force_matching`` on seeded random graphs.
+* ``training``  -- ``training.json``: sha256 of ``simenv.dataset_to_csv`` of
+  ``generate_dataset`` (simenv.py:393-469) for two (noise, seed, budget)
+  settings; ``fnn.backward`` (fnn.py:174-210) gradients and losses on seeded
+  batches; and a 20-epoch ``fnn.train`` (fnn.py:260-297) of the acceptance
+  recipe (history + final weights).
 """
 
 from __future__ import annotations
@@ -354,8 +359,40 @@ def stage_analytic():
         json.dump(doc, fh, indent=0, sort_keys=True)
 
 
+def stage_training():
+    import tempfile
+    doc = {"datasets": [], "backward": [], "train": {}}
+    for sigma, seed, budget in ((0.0, 0, 400.0), (0.05, 3, 350.0)):
+        ds = simenv.generate_dataset(simenv.OracleParams(noise_sigma=sigma, seed=seed),
+                                     core.default_space(budget))
+        path = os.path.join(tempfile.mkdtemp(), "d.csv")
+        simenv.dataset_to_csv(ds, path)
+        with open(path, "rb") as fh:
+            sha = hashlib.sha256(fh.read()).hexdigest()
+        doc["datasets"].append({"noise_sigma": sigma, "seed": seed, "p_total": budget,
+                                "rows": len(ds.rows), "csv_sha256": sha})
+    ds = simenv.generate_dataset(simenv.OracleParams(noise_sigma=0.0), core.default_space(400.0), seed=0)
+    train = ds.samples("train")
+    w0 = fnn.initialize_weights(5, ds.bounds)
+    for b, (start, size) in enumerate(((0, 1), (10, 4), (100, 32), (500, 77))):
+        batch = train[start:start + size]
+        g, loss = fnn.backward(w0, batch)
+        doc["backward"].append({"init_seed": 5, "start": start, "size": size, "loss": loss,
+                                **{k: getattr(g, k).tolist() for k in ("w1", "b1", "w2", "b2", "w_out", "b_out")}})
+    cfg = fnn.TrainingConfig(learning_rate=0.002, batch_size=2, epochs=20, seed=2,
+                             validation_fraction=0.05)
+    weights, hist = fnn.train(train, cfg, feature_bounds=ds.bounds)
+    doc["train"] = {"cfg": {"learning_rate": 0.002, "batch_size": 2, "epochs": 20, "seed": 2,
+                            "validation_fraction": 0.05},
+                    "history": [[h.epoch, h.train_mse, h.val_mse] for h in hist],
+                    **{k: getattr(weights, k).tolist() for k in ("w1", "b1", "w2", "b2", "w_out", "b_out")}}
+    with open(os.path.join(HERE, "training.json"), "w") as fh:
+        json.dump(doc, fh)
+
+
 STAGES = {
     "weights": stage_weights,
+    "training": stage_training,
     "workloads": stage_workloads,
     "paper20": stage_paper20,
     "matching": stage_matching,

@@ -13,12 +13,13 @@ from paper_2405_03831_b200 import _native as nat
 def _declared(header):
     text = open(os.path.join(ROOT, "include", header)).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^[A-Za-z_][\w \*]*?\b((?:cs|cm)_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^[A-Za-z_][\w \*]*?\b((?:cs|cm|ct)_\w+)\s*\(", text, flags=re.M)))
 
 
 @pytest.mark.parametrize("header,loader,table", [
     ("cosched_b200.h", nat.sweep_lib, nat.SWEEP_SYMBOLS),
     ("cosched_match.h", nat.match_lib, nat.MATCH_SYMBOLS),
+    ("cosched_train.h", nat.train_lib, nat.TRAIN_SYMBOLS),
 ])
 def test_every_declared_symbol_is_exported_and_bound(header, loader, table):
     names = _declared(header)
@@ -36,6 +37,12 @@ def test_sweep_library_is_sm100a_and_static_cudart():
     lib = nat.sweep_lib()
     assert lib.cs_version().decode().startswith("cosched_b200")
     assert lib.cs_error_string(-2).decode().startswith("no co-run configs")
+
+
+def test_train_library_is_sm100a():
+    blob = open(nat.TRAIN_LIB, "rb").read()
+    assert b"sm_100a" in blob
+    assert nat.train_lib().ct_version().decode().startswith("cosched_train")
 
 
 def test_host_only_layout_functions():

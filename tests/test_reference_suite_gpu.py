@@ -1,6 +1,6 @@
 """The reference's OWN unit tests, run against the drop-in on the GPU.
 
-``pkg/tests/test_{core,hwopt,estimator,scheduler,matcher}.py`` of the
+``pkg/tests/test_{core,hwopt,estimator,scheduler,matcher,fnn}.py`` of the
 unmodified reference are executed in a subprocess whose ``cosched`` package is
 the alias in ``tests/ref_alias`` (every ``cosched.X`` is the drop-in's module
 ``paper_2405_03831_b200.X``).  The test files are read from the staged copy
@@ -21,7 +21,7 @@ import pytest
 from conftest import ROOT
 
 CANDIDATES = (os.path.join(ROOT, "baseline", "_ref", "ref_tests"), "/root/reference/pkg/tests")
-SUITES = ("test_core", "test_hwopt", "test_estimator", "test_scheduler", "test_matcher")
+SUITES = ("test_core", "test_hwopt", "test_estimator", "test_scheduler", "test_matcher", "test_fnn")
 
 
 def _ref_tests():
