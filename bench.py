@@ -425,7 +425,7 @@ def roofline(name, kernel, kernel_ms, units, step_ms):
     achieved = FLOPS_PER_UNIT * units / (kernel_ms / 1e3) / 1e12
     return {"bound": "tensor", "achieved": achieved, "peak": tf, "unit": "TFLOP/s",
             "frac": achieved / tf, "traffic": measured_traffic(name, kernel),
-            "kernel": {"tcgen05": "k_sweep_tc3<L,4,2,3> (tcgen05, A in TMEM)",
+            "kernel": {"tcgen05": "k_sweep_tc3<L,4,2,515> (tcgen05, A in TMEM, TMA-staged tables, setmaxnreg)",
                        "simt": "k_sweep (SIMT fp32)"}[kernel],
             "kernel_ms": kernel_ms, "flops_per_unit": FLOPS_PER_UNIT,
             "units_per_launch": units, "unit_def": "unique (pair, config)",

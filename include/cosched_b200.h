@@ -113,7 +113,7 @@ typedef struct {
     uint16_t *w2_tile;            /* fp16 [W2hi|W2hi|W2lo|b2] B operand of the tcgen05 screen */
     float *app_a32, *app_b32;     /* N x 20 (18 + pad): primary / co-runner partials */
     double *app_a64, *app_b64;    /* 18 x N, chunk-major: [9][N] double2 */
-    float *knob1_32, *knob2_32;   /* G x 20, b1 folded */
+    float *knob1_32, *knob2_32;   /* b1 folded; [G][2][20], K1|K2 interleaved (row stride 40), knob2_32 = knob1_32 + 20 */
     double *knob1_64, *knob2_64;  /* b1 folded; [9][G][2] double2, K1|K2 interleaved, knob2_64 = knob1_64 + 2 */
     double *solo64;               /* S x 18, b1 folded */
     double *net_image;            /* the network in device memory (cs_tables_set_network) */

@@ -39,6 +39,7 @@ constexpr int NF = CS_NUM_FEATURES;
 constexpr int HD = CS_HIDDEN;
 constexpr int IN = CS_INPUT_DIM;
 constexpr int ROW32 = 20;                  // fp32 table row: 18 + 2 pad (80 B, float4-aligned)
+constexpr int KROW32 = 2 * ROW32;          // row stride of the interleaved K1|K2 fp32 knob table
 constexpr int W2_TILE_ELEMS = 4 * 32 * 16; // fp16 B operands: 4 K-slices of W2 (tcgen05_util.cuh)
 constexpr double FLOOR = 0.5;              // estimator.py:33
 constexpr int kSweepThreads = 128;
@@ -558,11 +559,11 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
             if (lane < HD) {
                 t.knob1_64[knob64_at(g.G, (int)c, 0, h)] = s1;
                 t.knob1_64[knob64_at(g.G, (int)c, 1, h)] = s2;
-                t.knob1_32[c * ROW32 + h] = (float)s1;
-                t.knob2_32[c * ROW32 + h] = (float)s2;
+                t.knob1_32[c * KROW32 + h] = (float)s1;
+                t.knob2_32[c * KROW32 + h] = (float)s2;
             } else if (lane < ROW32) {
-                t.knob1_32[c * ROW32 + lane] = 0.f;
-                t.knob2_32[c * ROW32 + lane] = 0.f;
+                t.knob1_32[c * KROW32 + lane] = 0.f;
+                t.knob2_32[c * KROW32 + lane] = 0.f;
             }
         } else {
             const int64_t c = r - n - g.G;
@@ -645,11 +646,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(const SweepArgs a,
         for (int c = s; c < a.g.G; c += S) {
             const uint32_t m = L == 1 ? 1u : __ldg(a.g.mask + c);
             float z[HD];
-            load_row20(a.t.knob1_32 + (size_t)c * ROW32, z);
+            load_row20(a.t.knob1_32 + (size_t)c * KROW32, z);
 #pragma unroll
             for (int h = 0; h < HD; ++h) z[h] += p1[h];
             const float y1 = head32(net, z);
-            load_row20(a.t.knob2_32 + (size_t)c * ROW32, z);
+            load_row20(a.t.knob2_32 + (size_t)c * KROW32, z);
 #pragma unroll
             for (int h = 0; h < HD; ++h) z[h] += p2[h];
             const float y2 = head32(net, z);
@@ -1121,9 +1122,11 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
     if (kind != CS_KERNEL_TCGEN05 && (kind & 0xF00) != 0x300) return CS_ERR_ARG;
     // default: 4 compute groups x 2 TMEM stages, per-group issuer warps,
-    // elected a_ready arrives (0x3342); 0xV3GS kinds select the timing-probe
-    // instances compiled with -DCS_TIMING_PROBES (tools/, never the product)
-    if (kind == CS_KERNEL_TCGEN05) kind = 0x3342;
+    // elected a_ready arrives, issuer registers handed to the compute warps
+    // by setmaxnreg (0x203342); other 0xV3GS kinds select the measured
+    // alternatives below and the timing-probe instances compiled with
+    // -DCS_TIMING_PROBES (tools/, never the product)
+    if (kind == CS_KERNEL_TCGEN05) kind = 0x203342;
     const int G = (kind >> 4) & 0xF, S = kind & 0xF;
     const size_t smem = tc3_smem_bytes(a.g.G);
     if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
@@ -1152,11 +1155,15 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
         }
         return CS_OK;
     };
-    const int V = (kind >> 12) & 0xFF;
+    const int V = (kind >> 12) & 0xFFF;
 #define CS_TC3(GG, SS, VV) \
     if (G == GG && S == SS && V == VV) \
         return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
     CS_TC3(4, 2, 3)
+    CS_TC3(4, 2, 11)
+    CS_TC3(4, 2, 259)
+    CS_TC3(4, 2, 515)
+    CS_TC3(4, 2, 547)
 #ifdef CS_TIMING_PROBES
     CS_TC3(4, 2, 19) CS_TC3(4, 2, 67) CS_TC3(4, 2, 131) CS_TC3(4, 2, 195)
 #endif
@@ -1211,8 +1218,10 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
     out->app_b32 = (float *)take(sizeof(float) * (size_t)n_apps * ROW32);
     out->app_a64 = (double *)take(sizeof(double) * (size_t)n_apps * HD);
     out->app_b64 = (double *)take(sizeof(double) * (size_t)n_apps * HD);
-    out->knob1_32 = (float *)take(sizeof(float) * (size_t)n_grid * ROW32);
-    out->knob2_32 = (float *)take(sizeof(float) * (size_t)n_grid * ROW32);
+    // fp32 knob rows of both members interleaved per config ([G][2][20]), so
+    // the screen stages the whole table with one bulk (TMA) copy
+    out->knob1_32 = (float *)take(2 * sizeof(float) * (size_t)n_grid * ROW32);
+    out->knob2_32 = out->knob1_32 + ROW32;
     // fp64 knob rows of both members interleaved per chunk (see knob64_at)
     out->knob1_64 = (double *)take(2 * sizeof(double) * (size_t)n_grid * HD);
     out->knob2_64 = out->knob1_64 + 2;

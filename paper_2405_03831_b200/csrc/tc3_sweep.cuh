@@ -49,6 +49,13 @@ struct Cfg {
 #else
     static constexpr bool kNoExact = false, kNoWrite = false;
 #endif
+    // bit 8: group g's compute warps start g quarter-periods late, so the
+    //        groups' MMA bursts reach the shared tensor pipe staggered
+    static constexpr bool kStagger = (V & 256) != 0;
+    // bit 9: register rebalancing -- the MMA-issuer warpgroup gives registers
+    //        back (setmaxnreg.dec 32), the compute warpgroups take them
+    //        (setmaxnreg.inc 112); needs G == 4 with per-group issuers
+    static constexpr bool kMaxNReg = (V & 512) != 0;
     static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
     static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
@@ -193,17 +200,19 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     constexpr int kThreads = C::kThreads;
     extern __shared__ __align__(1024) uint8_t smem[];
     // carve: [B slices 4 KB][K12: G_cfg x 2 x 20 fp32][mask G_cfg][d_ready G*S][a_ready G*S]
-    //        [tmem slot][Head64P][wo, bo fp32]
+    //        [staged][tmem slot][Head64P][wo, bo fp32]
     uint8_t *b_tile = smem;
     float *k12 = reinterpret_cast<float *>(smem + tc2::kBBytes);
     uint32_t *masks = reinterpret_cast<uint32_t *>(k12 + (size_t)a.g.G * 2 * ROW32);
     uint64_t *d_ready = reinterpret_cast<uint64_t *>(
         smem + ((reinterpret_cast<uint8_t *>(masks + a.g.G) - smem + 7) & ~ptrdiff_t(7)));
     uint64_t *a_ready = d_ready + G * S;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + G * S);
+    uint64_t *staged = a_ready + G * S;        // completion of the prologue's bulk copies
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(staged + 1);
     Head64P *net64 = reinterpret_cast<Head64P *>(
-        smem + ((reinterpret_cast<uint8_t *>(a_ready + G * S + 2) - smem + 15) & ~ptrdiff_t(15)));
+        smem + ((reinterpret_cast<uint8_t *>(staged + 3) - smem + 15) & ~ptrdiff_t(15)));
     float *wo_s = reinterpret_cast<float *>(net64 + 1);          // wo[18], bo
+    static_assert(sizeof(Head64P) % 16 == 0, "bulk-copy granule");
 
     const int tid = threadIdx.x;
     const int g = tid / tc::kGroupThreads;     // == G: the MMA-issuer warp
@@ -217,6 +226,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
             tc::mbar_init(&d_ready[i], 1);
             tc::mbar_init(&a_ready[i], C::kElected ? tc::kGroupThreads / 32 : tc::kGroupThreads);
         }
+        tc::mbar_init(staged, 1);
         tc::fence_mbar_init();
     }
     if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -226,28 +236,33 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     // take SMs this grid leaves free and stage their weights, then wait for
     // this grid to finish before reading the queue
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    for (int i = tid; i < tc2::kBBytes / 16; i += kThreads)
-        reinterpret_cast<uint4 *>(b_tile)[i] =
-            reinterpret_cast<const uint4 *>(a.t.w2_tile)[i];
-    for (int i = tid; i < a.g.G * ROW32; i += kThreads) {
-        const int c = i / ROW32, h = i - c * ROW32;
-        k12[(2 * c) * ROW32 + h] = a.t.knob1_32[i];
-        k12[(2 * c + 1) * ROW32 + h] = a.t.knob2_32[i];
+    // the per-sweep tables k_tables wrote -- the fp16 B operand (W2 split), the
+    // interleaved K1|K2 knob rows and the fp64 head -- are staged by TMA bulk
+    // copies issued by one thread, completing on `staged`
+    if (tid == 0) {
+        const uint32_t kbytes = (uint32_t)a.g.G * 2 * ROW32 * sizeof(float);
+        tc::mbar_expect_tx(staged, tc2::kBBytes + kbytes + (uint32_t)sizeof(Head64P));
+        tc::bulk_g2s(b_tile, a.t.w2_tile, tc2::kBBytes, staged);
+        tc::bulk_g2s(k12, a.t.knob1_32, kbytes, staged);
+        tc::bulk_g2s(net64, a.t.net_image + kImgHeadOff, (uint32_t)sizeof(Head64P), staged);
     }
     for (int i = tid; i < a.g.G; i += kThreads) masks[i] = L == 1 ? 1u : a.g.mask[i];
     // 0.5 wo (the |z2| half of the ReLU, see `math`) and bo
     if (tid <= HD) wo_s[tid] = tid < HD ? 0.5f * net.wo[tid] : net.bo;
-    for (int i = tid; i < (int)(sizeof(Head64P) / 8); i += kThreads)
-        reinterpret_cast<double *>(net64)[i] = __ldg(a.t.net_image + kImgHeadOff + i);
-    tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    tc::mbar_wait(staged, 0);
     const uint32_t tmem_base = *tmem_slot;
     const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
     const int64_t total_groups = (int64_t)gridDim.x * G;
     const int n_cfg = a.g.G;
 
+    if (C::kMaxNReg) {
+        static_assert(!C::kMaxNReg || (G == 4 && C::kPerGroupIssuer), "warpgroup-aligned roles");
+        if (g >= G) asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 112;" ::: "memory");
+    }
     if (C::kNoTensor && g >= G) {
         // timing probe: CUDA-core work only (results are garbage)
     } else if (!C::kComputeIssue && g >= G) {
@@ -300,6 +315,10 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
 #pragma unroll
         for (int l = 0; l < L; ++l) clamps[l] = 0;
         const int member = t & 1;
+        if (C::kStagger && g > 0) {
+            const long long t0 = clock64();
+            while (clock64() - t0 < (long long)g * 224) {}
+        }
 
         for (int64_t blk = (int64_t)blockIdx.x * G + g; blk < nblocks; blk += total_groups) {
             const int64_t pl = blk * tc::kPairsPerBlock + (t >> 1);
@@ -478,6 +497,6 @@ inline size_t tc3_smem_bytes(int n_grid) {
     size_t b = (size_t)tc2::kBBytes;
     b += 2 * (size_t)n_grid * ROW32 * sizeof(float) + (size_t)n_grid * sizeof(uint32_t);
     b = (b + 7) & ~(size_t)7;
-    b += 2 * 16 * sizeof(uint64_t) + 32 + sizeof(Head64P) + 20 * sizeof(float);
+    b += 2 * 16 * sizeof(uint64_t) + 3 * sizeof(uint64_t) + 16 + sizeof(Head64P) + 20 * sizeof(float);
     return b;
 }

@@ -15,6 +15,7 @@ size) launch kernels only:
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from dataclasses import dataclass
 from typing import Optional
@@ -146,6 +147,9 @@ class SweepPlan:
             # (identical results: the exact fp64 steps are shared)
             kernel = "simt"
         self.kernel, self.kernel_kind = kernel, kinds[kernel]
+        if kernel == "tcgen05" and os.environ.get("COSCHED_TC_KIND"):
+            # experiment hook: an explicit k_sweep_tc3 instance (0xV3GS kind code)
+            self.kernel_kind = int(os.environ["COSCHED_TC_KIND"], 16)
         self.pair_begin, self.pair_end = int(pair_begin), pair_end
         self.P = pair_end - pair_begin
         self.net = NetworkABI(weights)
