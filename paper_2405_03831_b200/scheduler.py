@@ -20,7 +20,9 @@ from typing import Sequence
 import numpy as np
 
 from . import analytic, estimator
-from .core import ConfigSpace, HardwareConfig, JobSet, Schedule, SchedulingParams, ValidationError, solo_config
+from .core import (ConfigSpace, HardwareConfig, JobSet, Schedule, SchedulingParams, ValidationError,
+                   normalize_input, solo_config)
+from .fnn import forward_batch
 from .hwopt import PairDecision, decide_pair
 from .matcher import PairGraph, min_weight_perfect_matching
 
@@ -186,18 +188,58 @@ def set_time(model, js: JobSet, configs: Sequence, corun: bool, space: ConfigSpa
     return estimator.solo_app_time(model, js.jobs[0], hc.cpu_cap, hc.gpu_cap, space)
 
 
+def _set_times(sched: Schedule, model, space: ConfigSpace, passes: int = 1) -> list:
+    """set_time of every emitted set.  For a trained network all the set's
+    slowdown queries (two per co-run set, member 2 on reversed partitions; one
+    per solo set) go to the GPU as ONE forward_batch instead of a device round
+    trip per query; floors, clamp counting (``passes`` times, as often as the
+    reference evaluates each query) and the max / sum are applied on the host
+    in the reference's order, so the values equal the scalar path's."""
+    weights = estimator.fnn_weights_of(model)
+    if weights is None:
+        out = [set_time(model, js, cs, fl, space)
+               for js, cs, fl in zip(sched.job_sets, sched.configs, sched.corun_flags)]
+        for _ in range(passes - 1):
+            for js, cs, fl in zip(sched.job_sets, sched.configs, sched.corun_flags):
+                set_time(model, js, cs, fl, space)
+        return out
+    rows, owners = [], []
+    for k, (js, cs, fl) in enumerate(zip(sched.job_sets, sched.configs, sched.corun_flags)):
+        hc = cs[0]
+        if fl:
+            if len(js) == 1:
+                rows.append(normalize_input(js.jobs[0], None, hc, space, weights.feature_bounds))
+                owners.append((k, 0))
+            else:
+                for m in range(len(js)):
+                    view = hc if m == 0 else hc.reversed_partitions()
+                    rows.append(normalize_input(js.jobs[m], js.jobs[1 - m], view, space,
+                                                weights.feature_bounds))
+                    owners.append((k, m))
+        else:
+            rows.append(normalize_input(js.jobs[0], None, solo_config(hc.cpu_cap, hc.gpu_cap),
+                                        space, weights.feature_bounds))
+            owners.append((k, 0))
+    preds = forward_batch(weights, np.stack(rows)) if rows else np.zeros(0)
+    floor = estimator.SLOWDOWN_FLOOR
+    estimator.clamp_stats.count += passes * int(np.count_nonzero(preds < floor))
+    member_times: dict = {}
+    for (k, m), y in zip(owners, preds):
+        y = float(y)
+        member_times.setdefault(k, []).append((floor if y < floor else y) * sched.job_sets[k].jobs[m].base_time)
+    return [max(member_times[k]) for k in range(len(sched.job_sets))]
+
+
 def predicted_makespan(sched: Schedule, model, space: ConfigSpace) -> float:
-    return sum(set_time(model, js, cs, fl, space)
-               for js, cs, fl in zip(sched.job_sets, sched.configs, sched.corun_flags))
+    return sum(_set_times(sched, model, space))
 
 
 def schedule_to_json(sched: Schedule, model, space: ConfigSpace) -> dict:
+    times = _set_times(sched, model, space, passes=2)   # set loop + predicted_makespan
     sets = [{"jobs": [job.job_id for job in js.jobs], "corun": bool(fl),
-             "configs": [hc.to_json() for hc in cs],
-             "predicted_s": set_time(model, js, cs, fl, space)}
-            for js, cs, fl in zip(sched.job_sets, sched.configs, sched.corun_flags)]
-    return {"p_total_w": space.p_total, "sets": sets,
-            "total_predicted_s": predicted_makespan(sched, model, space)}
+             "configs": [hc.to_json() for hc in cs], "predicted_s": t}
+            for js, cs, fl, t in zip(sched.job_sets, sched.configs, sched.corun_flags, times)]
+    return {"p_total_w": space.p_total, "sets": sets, "total_predicted_s": sum(times)}
 
 
 def write_schedule_json(sched: Schedule, model, space: ConfigSpace, path) -> None:

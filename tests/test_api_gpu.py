@@ -120,3 +120,27 @@ def test_graph_csv_fast_path_matches_generic(tmp_path, weights):
     plain = cs.PairGraph(g.weights, {k: g.decisions[k] for k in g.decisions})
     cs.matcher.graph_to_csv(plain, slow)
     assert fast.read_text() == slow.read_text()
+
+
+def test_batched_set_times_equal_the_scalar_path(weights):
+    """predicted_makespan / schedule_to_json send every set's slowdown queries
+    to the GPU as one forward_batch; the times, their sum and the clamp counter
+    must equal the reference-shaped scalar path (one query per call)."""
+    from paper_2405_03831_b200 import scheduler
+    n = 96
+    jobs = synth.generate_jobs(3, synth.mixed_archetypes(n))
+    space = core.default_space(350.0)
+    inp = cs.SchedulerInput(tuple(jobs), space, core.SchedulingParams(window=n), weights)
+    sched = cs.schedule(inp)
+    assert any(sched.corun_flags) and not all(sched.corun_flags)
+    estimator.clamp_stats.reset()
+    scalar = [scheduler.set_time(weights, js, c, f, space)
+              for js, c, f in zip(sched.job_sets, sched.configs, sched.corun_flags)]
+    c_scalar = estimator.clamp_stats.count
+    estimator.clamp_stats.reset()
+    assert scheduler._set_times(sched, weights, space) == scalar
+    assert estimator.clamp_stats.count == c_scalar
+    assert cs.predicted_makespan(sched, weights, space) == sum(scalar)
+    doc = cs.schedule_to_json(sched, estimator.FnnSlowdownModel(weights), space)
+    assert [s["predicted_s"] for s in doc["sets"]] == scalar
+    assert doc["total_predicted_s"] == sum(scalar)
