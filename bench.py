@@ -609,6 +609,7 @@ def run_ours(args):
                 subs[sub] = measure_single(args, sub, 10, 3, dev, weights, 1,
                                            e2e=not args.no_e2e, schedule=not args.no_e2e)
             line["workloads"] = subs
+            line["training"] = measure_training(not args.no_cpu_baseline)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(weights, name, seconds=args.cpu_seconds)
             ref = cpu_baseline_reference(name)
@@ -617,6 +618,49 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
         return
     run_multi(args, name, world, rank, local_rank, dev, weights)
+
+
+def measure_training(with_reference: bool):
+    """the acceptance training recipe (test_acceptance.py:
+    144-157 -- 2,400-row corpus, lr 0.002, batch 2, 400 epochs, seed 2) on the
+    device trainer (one persistent CTA), plus 148 seeds at once (one per SM),
+    next to the unmodified reference's numpy loop on a bounded number of
+    epochs (baseline/_ref, when staged)."""
+    import torch
+    from paper_2405_03831_b200 import analytic, core as _core, fnn, simenv
+    from paper_2405_03831_b200.trainer import train_many
+    ds = simenv.generate_dataset(analytic.OracleParams(noise_sigma=0.0), _core.default_space(400.0), seed=0)
+    data = ds.samples("train")
+    kw = dict(learning_rate=0.002, batch_size=2, seed=2, validation_fraction=0.05)
+    fnn.train(data, fnn.TrainingConfig(epochs=1, **kw), ds.bounds)          # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, hist = fnn.train(data, fnn.TrainingConfig(epochs=400, **kw), ds.bounds)
+    t1 = time.perf_counter()
+    n_train = len(data) - int(len(data) * 0.05)
+    steps = 400 * ((n_train + 1) // 2)
+    out = {"recipe": "generate_dataset(sigma 0, 400 W, seed 0) train rows; lr 0.002, batch 2, "
+                     "400 epochs, seed 2, val 0.05",
+           "train_rows": n_train, "sgd_steps": steps, "device_s": t1 - t0,
+           "device_sgd_steps_per_s": steps / (t1 - t0), "final_train_mse": hist[-1].train_mse}
+    cfgs = [fnn.TrainingConfig(epochs=400, **{**kw, "seed": s}) for s in range(148)]
+    t0 = time.perf_counter()
+    train_many(data, cfgs, ds.bounds)
+    out["train_many"] = {"runs": 148, "s": time.perf_counter() - t0}
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if with_reference and os.path.isdir(os.path.join(ref, "cosched")):
+        code = ("import sys, time; sys.path.insert(0, %r)\n"
+                "from cosched import fnn, simenv, core\n"
+                "ds = simenv.generate_dataset(simenv.OracleParams(noise_sigma=0.0), core.default_space(400.0), seed=0)\n"
+                "cfg = fnn.TrainingConfig(learning_rate=0.002, batch_size=2, epochs=10, seed=2, validation_fraction=0.05)\n"
+                "t0 = time.perf_counter(); fnn.train(ds.samples('train'), cfg, feature_bounds=ds.bounds)\n"
+                "print(time.perf_counter() - t0)\n") % ref
+        res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+        if res.returncode == 0:
+            s10 = float(res.stdout.strip().splitlines()[-1])
+            out["reference"] = {"epochs_timed": 10, "s": s10, "s_400_epochs_extrapolated": s10 * 40,
+                                "api": "unmodified cosched.fnn.train (numpy, 1 process)"}
+    return out
 
 
 def run_multi(args, name, world, rank, local_rank, dev, weights):

@@ -13,4 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 2 -c 1 -o $OUT/prof_sweep_$TAG -f \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1
-echo done
+
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 1 -c 1 -o $OUT/prof_sweep4096_$TAG -f \
+  python bench.py --workload n4096 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-subresults > $OUT/ncu_full4096_$TAG.log 2>&1
+echo done4096
