@@ -117,6 +117,11 @@ typedef struct {
     double *knob1_64, *knob2_64;  /* b1 folded; [9][G][2] double2, K1|K2 interleaved, knob2_64 = knob1_64 + 2 */
     double *solo64;               /* S x 18, b1 folded */
     double *net_image;            /* the network in device memory (cs_tables_set_network) */
+    float *split_scratch;         /* tcgen05 screen, stream-K: partial argmins of work items
+                                     cut between group slots, [slots][2][3L+1][128] */
+    uint32_t *split_cnt;          /* per slot: pieces of its split item seen so far (zeroed
+                                     by cs_prepare, left zero by the screen) */
+    int32_t split_slots;          /* capacity of the two arrays above (group slots) */
 } cs_tables;
 
 /* Per-pair outputs of one shard, budget-major: element [l * P + (p - pair_begin)]. */

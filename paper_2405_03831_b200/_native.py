@@ -61,7 +61,8 @@ class CsTables(ctypes.Structure):
                 ("app_a64", c_double_p), ("app_b64", c_double_p),
                 ("knob1_32", c_float_p), ("knob2_32", c_float_p),
                 ("knob1_64", c_double_p), ("knob2_64", c_double_p), ("solo64", c_double_p),
-                ("net_image", c_double_p)]
+                ("net_image", c_double_p), ("split_scratch", c_float_p),
+                ("split_cnt", c_uint32_p), ("split_slots", ctypes.c_int32)]
 
 
 class CsPairOut(ctypes.Structure):

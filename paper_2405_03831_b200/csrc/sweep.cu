@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
         if (reset_cnt && threadIdx.x < (int)(sizeof(cs_counters) / 4))
             reinterpret_cast<uint32_t *>(reset_cnt)[threadIdx.x] = 0u;
         if (reset_clamps && threadIdx.x < g.L) reset_clamps[threadIdx.x] = 0ull;
+        for (int i = threadIdx.x; i < t.split_slots; i += blockDim.x) t.split_cnt[i] = 0u;
     }
     __syncthreads();
     const Net64P &net = sm.net;
@@ -1074,6 +1075,15 @@ int sm_count() {
     return sms > 0 ? sms : 148;
 }
 
+// stream-K split scratch of the tcgen05 screen: one slot per (CTA, group) of
+// a full-device grid, two pieces per slot, 3L+1 fields (L <= 8) x 128 threads
+constexpr int kMaxSplitSlots = 4 * 256;
+int split_slots() {
+    const int s = 4 * sm_count();
+    return s < kMaxSplitSlots ? s : kMaxSplitSlots;
+}
+size_t split_scratch_floats() { return (size_t)split_slots() * 2 * (3 * CS_MAX_BUDGETS + 1) * 128; }
+
 int check_launch() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -1123,11 +1133,16 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
     if (kind != CS_KERNEL_TCGEN05 && (kind & 0xF00) != 0x300) return CS_ERR_ARG;
     // default: 4 compute groups x 2 TMEM stages, per-group issuer warps,
     // elected a_ready arrives, issuer registers handed to the compute warps
-    // by setmaxnreg (0x203342); other 0xV3GS kinds select the measured
-    // alternatives below and the timing-probe instances compiled with
-    // -DCS_TIMING_PROBES (tools/, never the product)
+    // by setmaxnreg, whole items round-robin (0x203342); the stream-K schedule
+    // (0xA03342) measured slower (the extra fp64 tails of split items cost
+    // more than the idle SMs it fills); other 0xV3GS kinds select
+    // the measured alternatives below and the timing-probe instances compiled
+    // with -DCS_TIMING_PROBES (tools/build_probes.sh, never the product)
     if (kind == CS_KERNEL_TCGEN05) kind = 0x203342;
     const int G = (kind >> 4) & 0xF, S = kind & 0xF;
+    int V = (kind >> 12) & 0xFFF;
+    // stream-K keeps its schedule arithmetic in 32 bits
+    if ((V & 2048) && nblocks * (int64_t)a.g.G >= ((int64_t)1 << 31)) V &= ~2048;
     const size_t smem = tc3_smem_bytes(a.g.G);
     if (smem > 227 * 1024) return CS_ERR_ARG;   // grid too large for the staged K tables
     auto go3 = [&](auto kern, int groups, int threads) -> int {
@@ -1135,7 +1150,14 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
             cudaSuccess)
             return CS_ERR_CUDA;
         int64_t c = (nblocks + groups - 1) / groups;
+        if (V & 2048) {
+            // stream-K: every SM, as long as a group slot keeps >= 32 configs
+            const int64_t work = nblocks * (int64_t)a.g.G;
+            c = (work + (int64_t)groups * 32 - 1) / ((int64_t)groups * 32);
+            if (c * groups > a.t.split_slots) c = a.t.split_slots / groups;
+        }
         if (c > sm_count()) c = sm_count();
+        if (c < 1) c = 1;
         // programmatic dependent launch: the CTAs' prologue (TMEM allocation,
         // mbarrier init) overlaps the tail of k_tables; the kernel waits on
         // griddepcontrol.wait before it reads anything k_tables wrote
@@ -1155,17 +1177,14 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
         }
         return CS_OK;
     };
-    const int V = (kind >> 12) & 0xFFF;
 #define CS_TC3(GG, SS, VV) \
     if (G == GG && S == SS && V == VV) \
         return go3(k_sweep_tc3<L, GG, SS, VV>, GG, tc3::Cfg<GG, SS, VV>::kThreads);
-    CS_TC3(4, 2, 3)
-    CS_TC3(4, 2, 11)
-    CS_TC3(4, 2, 259)
-    CS_TC3(4, 2, 515)
-    CS_TC3(4, 2, 547)
+    CS_TC3(4, 2, 515)    // default: setmaxnreg, round-robin whole items
+    CS_TC3(4, 2, 2563)   // setmaxnreg + stream-K
+    CS_TC3(4, 2, 3)      // round-robin, no register rebalancing
 #ifdef CS_TIMING_PROBES
-    CS_TC3(4, 2, 19) CS_TC3(4, 2, 67) CS_TC3(4, 2, 131) CS_TC3(4, 2, 195)
+    CS_TC3(4, 2, 531) CS_TC3(4, 2, 579) CS_TC3(4, 2, 595)
 #endif
 #undef CS_TC3
     return CS_ERR_ARG;
@@ -1203,6 +1222,8 @@ size_t cs_tables_bytes(int32_t n_apps, int32_t n_grid, int32_t n_solo) {
     b += 2 * align256(sizeof(double) * (size_t)n_grid * HD);
     b += align256(sizeof(double) * (size_t)n_solo * HD);
     b += align256(sizeof(double) * (size_t)kImgDoubles);
+    b += align256(sizeof(float) * split_scratch_floats());
+    b += align256(sizeof(uint32_t) * (size_t)split_slots());
     return b;
 }
 
@@ -1227,6 +1248,9 @@ int cs_tables_bind(void *d_base, size_t bytes, int32_t n_apps, int32_t n_grid, i
     out->knob2_64 = out->knob1_64 + 2;
     out->solo64 = (double *)take(sizeof(double) * (size_t)n_solo * HD);
     out->net_image = (double *)take(sizeof(double) * (size_t)kImgDoubles);
+    out->split_scratch = (float *)take(sizeof(float) * split_scratch_floats());
+    out->split_cnt = (uint32_t *)take(sizeof(uint32_t) * (size_t)split_slots());
+    out->split_slots = split_slots();
     return CS_OK;
 }
 

@@ -1,63 +1,60 @@
-// tc3_sweep.cuh -- tcgen05 screen, v4: the v3 (tc2) pipeline on an instruction diet.
+// tc3_sweep.cuh -- the tcgen05 screen (k_sweep_tc3): pair x knob tiles through
+// layer 2 of the network on the tensor cores, fused with the floor, the
+// objective, the per-budget argmin and the exact fp64 winner.
 //
-// Same math, TMEM map and result contract as k_sweep_tc2 (A operand in TMEM,
-// fp16 3-term split, 5 x tcgen05.mma M=128 N=32 K=16, fp32 epilogue, fp64
-// re-evaluation of the winner).  Profiling tc2 (profiles/r1a_sweep_ncu.md)
-// showed CUDA-core issue as the binding limit: 196 warp instructions per
-// (warp, config) where ~115 are the math itself.  This version removes the
-// rest:
-//   * the config loop is unrolled over the S pipeline stages, so every TMEM
-//     address, mbarrier address and phase bit is a compile-time offset;
-//   * G compute groups share ONE MMA-issuer warp (lockstep over groups), so
-//     G = 3 fits 4 warps per scheduler and 128 registers per thread;
-//   * every compute thread arrives on a_ready itself (count 128): no
-//     __syncwarp + elected arrive per config;
-//   * the MMA-issuer warps sleep in mbarrier.try_wait with a suspend-time hint
-//     instead of spinning on the issue slots the compute warps need;
-//   * the K1/K2 rows of a config are interleaved ([c][member][20]) so both
-//     member lanes of a warp read one 160-byte line;
-//   * floor clamps are counted per block and masked by `live` once per block.
+// Per CTA: G = 4 compute warpgroups ("groups", 128 threads: TMEM lane r = pair
+// r/2 of the group's 64-pair work item, member r%2) and one MMA-issuer warp
+// per group.  Per config the group's threads build their A rows (layer-1
+// ReLU, fp16 hi/lo split) straight into TMEM, the issuer warp's elected lane
+// issues 4 x tcgen05.mma M128 N32 K16 (A in TMEM, B = the W2 split in SMEM),
+// and the epilogue reads D back with tcgen05.ld for the head and the argmin.
+// S = 2 TMEM stages pipeline build(c) against epilogue(c - 1).
+//
+// Instruction diet (CUDA-core issue is the binding limit, profiles/r2*):
+//   * the config loop is unrolled over the S stages, so every TMEM address,
+//     mbarrier address and phase bit is a compile-time offset;
+//   * one elected arrive per warp on a_ready; the issuer warps sleep in
+//     mbarrier.try_wait with a suspend-time hint;
+//   * the K1/K2 rows of a config are interleaved ([c][member][20], one TMA
+//     bulk copy) so both member lanes of a warp read one 160-byte line;
+//   * setmaxnreg moves the issuer warpgroup's registers to the compute
+//     warpgroups (32 / 112).
+//
+// Work schedule (V bit 11, "stream-K"): the G x gridDim group slots split the
+// flattened (work item, config) space into equal contiguous ranges, so every
+// SM gets the same number of config steps even when there are fewer work
+// items than slots (256 apps: 510 items for 592 slots).  An item cut between
+// slots is finished by the LAST of its pieces to arrive: each piece leaves its
+// partial (min, first index, runner-up, smallest prediction) per thread in
+// the split scratch (cs_tables.split_scratch), bumps the item's counter, and
+// the last one merges the pieces in config order -- the same first-index
+// argmin -- then runs the exact tail.  Without bit 11 each slot takes whole
+// items round-robin.
 #pragma once
 
 namespace tc3 {
 
-// V bit 0: one elected arrive per warp on a_ready (count 4) instead of all
-//           128 threads arriving;
-// V bit 1: one MMA-issuer warp per group instead of one shared issuer;
-// V bit 2: no issuer warps -- the group's own compute warps take turns (warp
-//          c % 4 issues config c), so 4 warps per scheduler get 128 registers;
-// V bit 3: the issuer warps poll a_ready (try_wait without a suspend hint).
+// V bit 0: one elected arrive per warp on a_ready (count 4);
+// V bit 1: one MMA-issuer warp per group;
+// V bit 9: setmaxnreg register rebalancing (issuers 32, compute 112);
+// V bit 11: stream-K work schedule (above).
+// Timing probes (tools/build_probes.sh, -DCS_TIMING_PROBES; WRONG results by
+// design, never in the product .so): bit 4 no MMAs / waits, bit 6 no fp64
+// winner re-evaluation, bit 7 no record / matrix writes.
 template <int G, int S, int V = 0>
 struct Cfg {
-    static constexpr bool kElected = (V & 1) != 0;
-    static constexpr bool kPerGroupIssuer = (V & 2) != 0;
-    static constexpr bool kComputeIssue = (V & 4) != 0;
-    static constexpr bool kIssuerSpin = (V & 8) != 0;   // issuer polls instead of sleeping
+    static constexpr bool kMaxNReg = (V & 512) != 0;
+    static constexpr bool kStreamK = (V & 2048) != 0;
 #ifdef CS_TIMING_PROBES
-    static constexpr bool kNoTensor = (V & 16) != 0;    // TIMING PROBE ONLY: no MMAs, no waits
-#else
-    static constexpr bool kNoTensor = false;            // probes exist only in tool builds
-#endif
-    // bit 5: read D(c) into registers, then build A(c+S) into the freed stage
-    // BEFORE the epilogue math of c -- MMA(c+S) is issued one epilogue earlier
-    static constexpr bool kEarlyIssue = (V & 32) != 0;
-    // TIMING PROBES ONLY (wrong results): bit 6 skips the fp64 winner
-    // re-evaluation, bit 7 skips the record / matrix writes of the tail
-#ifdef CS_TIMING_PROBES
+    static constexpr bool kNoTensor = (V & 16) != 0;
     static constexpr bool kNoExact = (V & 64) != 0;
     static constexpr bool kNoWrite = (V & 128) != 0;
 #else
-    static constexpr bool kNoExact = false, kNoWrite = false;
+    static constexpr bool kNoTensor = false, kNoExact = false, kNoWrite = false;
 #endif
-    // bit 8: group g's compute warps start g quarter-periods late, so the
-    //        groups' MMA bursts reach the shared tensor pipe staggered
-    static constexpr bool kStagger = (V & 256) != 0;
-    // bit 9: register rebalancing -- the MMA-issuer warpgroup gives registers
-    //        back (setmaxnreg.dec 32), the compute warpgroups take them
-    //        (setmaxnreg.inc 112); needs G == 4 with per-group issuers
-    static constexpr bool kMaxNReg = (V & 512) != 0;
-    static constexpr int kIssuers = kComputeIssue ? 0 : kPerGroupIssuer ? G : 1;
-    static constexpr int kThreads = G * tc::kGroupThreads + kIssuers * 32;
+    static_assert((V & 3) == 3, "elected arrives and per-group issuer warps");
+    static_assert(!kMaxNReg || G == 4, "warpgroup-aligned roles for setmaxnreg");
+    static constexpr int kThreads = G * tc::kGroupThreads + G * 32;
     static_assert(G * S * 56 <= 512, "TMEM holds 512 columns");
     __device__ static constexpr uint32_t d_col(int g, int s) { return (uint32_t)((g * S + s) * 32); }
     __device__ static constexpr uint32_t a_col(int g, int s) {
@@ -96,10 +93,6 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t *bar, uint32_t parity) {
     while (!__all_sync(0xffffffffu, tc::mbar_try(bar, parity))) {
         if (clock64() - t0 > 4000000000LL) __trap();
     }
-}
-
-__device__ __forceinline__ void mbar_arrive_all(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
 
 // tcgen05.st of the 20 live A columns as 8 + 8 + 4 (smaller register blocks
@@ -141,8 +134,6 @@ __device__ __forceinline__ void issue_config(uint32_t d_t, uint32_t a_t, uint64_
         : "memory");
 }
 
-// this thread's A row of one config (20 live 32-bit TMEM columns, layout of
-// tcgen05_util.cuh), stored into its TMEM lane
 __device__ __forceinline__ float4 lds4(uint32_t a) {
     float4 v;
     asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -154,8 +145,10 @@ __device__ __forceinline__ float2 lds2(uint32_t a) {
     return v;
 }
 
-// krow: 32-bit shared-window address of this member's K row (a plain
-// integer, so ptxas never re-derives the generic->shared mapping in the loop)
+// this thread's A row of one config (20 live 32-bit TMEM columns, layout of
+// tcgen05_util.cuh), stored into its TMEM lane.  krow: 32-bit shared-window
+// address of this member's K row (a plain integer, so ptxas never re-derives
+// the generic->shared mapping in the loop)
 __device__ __forceinline__ void build_row(const float2 (&p2)[9], uint32_t krow, uint32_t taddr) {
     const float4 q0 = lds4(krow), q1 = lds4(krow + 16), q2 = lds4(krow + 32), q3 = lds4(krow + 48);
     const float2 q4 = lds2(krow + 64);
@@ -190,6 +183,55 @@ __device__ __forceinline__ float2 lds_f32x2(const float *p) {
     return v;
 }
 
+__device__ __forceinline__ void group_sync(int g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(tc::kGroupThreads) : "memory");
+}
+
+// The work of one group slot: contiguous segments (work item, [c0, c1)).
+// All stream-K arithmetic is 32-bit (the launcher keeps W = items x configs
+// below 2^31): 64-bit divisions compile to calls that spill the live state.
+struct Schedule {
+    int64_t nblocks, T64, blk;    // round-robin: items, slots, next item
+    uint32_t T, k, n_cfg;         // slots, this slot, configs per item
+    uint32_t W, q, r;             // stream-K: W = items * n_cfg = q * T + r
+    uint32_t pos, end;
+    bool stream_k;
+    // start of slot kk's range: floor(kk * W / T) exactly, as kk q + kk r / T
+    __device__ uint32_t bound(uint32_t kk) const { return kk * q + (kk * r) / T; }
+    // the slot whose range holds flattened position x
+    __device__ uint32_t slot_of(uint32_t x) const {
+        uint32_t kk = (uint32_t)((float)x * ((float)T / (float)W));
+        if (kk >= T) kk = T - 1;
+        while (kk + 1 < T && bound(kk + 1) <= x) ++kk;
+        while (kk > 0 && bound(kk) > x) --kk;
+        return kk;
+    }
+    __device__ void init() {
+        if (stream_k) { pos = bound(k); end = bound(k + 1); }
+        else blk = k;
+    }
+    __device__ bool next(int64_t &item, int &c0, int &c1) {
+        if (stream_k) {
+            if (pos >= end) return false;
+            const uint32_t it = pos / n_cfg;
+            item = it;
+            c0 = (int)(pos - it * n_cfg);
+            c1 = (int)(c0 + (end - pos) < n_cfg ? c0 + (end - pos) : n_cfg);
+            pos += (uint32_t)(c1 - c0);
+            return true;
+        }
+        if (blk >= nblocks) return false;
+        item = blk;
+        c0 = 0;
+        c1 = (int)n_cfg;
+        blk += T64;
+        return true;
+    }
+    // which of slot kk's two scratch sides holds its piece of `item`:
+    // 0 = the first segment of its range, 1 = the last
+    __device__ int side(uint32_t kk, uint32_t item) const { return bound(kk) / n_cfg == item ? 0 : 1; }
+};
+
 }  // namespace tc3
 
 template <int L, int G, int S, int V>
@@ -199,10 +241,11 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     using C = tc3::Cfg<G, S, V>;
     constexpr int kThreads = C::kThreads;
     extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ int s_last[G];                 // stream-K: this group finishes the item
     // carve: [B slices 4 KB][K12: G_cfg x 2 x 20 fp32][mask G_cfg][d_ready G*S][a_ready G*S]
     //        [staged][tmem slot][Head64P][wo, bo fp32]
     uint8_t *b_tile = smem;
-    float *k12 = reinterpret_cast<float *>(smem + tc2::kBBytes);
+    float *k12 = reinterpret_cast<float *>(b_tile + tc2::kBBytes);
     uint32_t *masks = reinterpret_cast<uint32_t *>(k12 + (size_t)a.g.G * 2 * ROW32);
     uint64_t *d_ready = reinterpret_cast<uint64_t *>(
         smem + ((reinterpret_cast<uint8_t *>(masks + a.g.G) - smem + 7) & ~ptrdiff_t(7)));
@@ -215,7 +258,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     static_assert(sizeof(Head64P) % 16 == 0, "bulk-copy granule");
 
     const int tid = threadIdx.x;
-    const int g = tid / tc::kGroupThreads;     // == G: the MMA-issuer warp
+    const int g = tid / tc::kGroupThreads;     // == G: the MMA-issuer warpgroup
     const int t = tid % tc::kGroupThreads;
     const int warp = tid >> 5;
     const int lane = tid & 31;
@@ -224,7 +267,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     if (tid == 0) {
         for (int i = 0; i < G * S; ++i) {
             tc::mbar_init(&d_ready[i], 1);
-            tc::mbar_init(&a_ready[i], C::kElected ? tc::kGroupThreads / 32 : tc::kGroupThreads);
+            tc::mbar_init(&a_ready[i], tc::kGroupThreads / 32);
         }
         tc::mbar_init(staged, 1);
         tc::fence_mbar_init();
@@ -254,58 +297,57 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
     tc::fence_after();
     tc::mbar_wait(staged, 0);
     const uint32_t tmem_base = *tmem_slot;
-    const int64_t nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
-    const int64_t total_groups = (int64_t)gridDim.x * G;
     const int n_cfg = a.g.G;
+    tc3::Schedule sched;
+    sched.nblocks = (a.P + tc::kPairsPerBlock - 1) / tc::kPairsPerBlock;
+    sched.T = gridDim.x * G;
+    sched.T64 = sched.T;
+    sched.k = blockIdx.x * G + (g < G ? g : warp - G * (tc::kGroupThreads / 32));
+    sched.n_cfg = (uint32_t)n_cfg;
+    sched.W = (uint32_t)(sched.nblocks * n_cfg);        // < 2^31 (launcher)
+    sched.q = sched.W / sched.T;
+    sched.r = sched.W - sched.q * sched.T;
+    sched.stream_k = C::kStreamK;
+    sched.init();
 
-    if (C::kMaxNReg) {
-        static_assert(!C::kMaxNReg || (G == 4 && C::kPerGroupIssuer), "warpgroup-aligned roles");
-        if (g >= G) asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
-        else asm volatile("setmaxnreg.inc.sync.aligned.u32 112;" ::: "memory");
-    }
-    if (C::kNoTensor && g >= G) {
-        // timing probe: CUDA-core work only (results are garbage)
-    } else if (!C::kComputeIssue && g >= G) {
-        // ===== one MMA-issuer warp serves the G groups in lockstep =====
-        // Every active group of a round sweeps the same configs in the same
-        // order, so the issuer visits (config k, group q) round-robin.
+    // setmaxnreg sits at the head of each role's branch: code after it that
+    // both roles share would be register-allocated for the smaller budget
+    if (g >= G) {
+        // ===== MMA-issuer warp q serves group q: the same segments, in order =====
+        if (C::kMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
         const uint32_t b_addr = tc::smem_u32(b_tile);
         const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
                        bq2 = tc2::slice_desc(b_addr + 2048);
-        uint32_t ph = 0;                               // bit q*S+s: parity of a_ready[q][s]
-        // per-group issuers: warp G*4 + q serves only group q
-        const int q_lo = C::kPerGroupIssuer ? warp - G * (tc::kGroupThreads / 32) : 0;
-        for (int64_t blk0 = (int64_t)blockIdx.x * G; blk0 < nblocks; blk0 += total_groups) {
-            const int active = nblocks - blk0 < G ? (int)(nblocks - blk0) : G;
-            const int q_hi = C::kPerGroupIssuer ? (q_lo < active ? q_lo + 1 : q_lo) : active;
-            int st = 0;
-            for (int k = 0; k < n_cfg; ++k) {
-                for (int q = q_lo; q < q_hi; ++q) {
+        if (C::kNoTensor) {
+            // timing probe: CUDA-core work only (results are garbage)
+        } else {
+            const int q = warp - G * (tc::kGroupThreads / 32);
+            uint32_t ph = 0;                           // bit s: parity of a_ready[q][s]
+            int64_t item;
+            int c0, c1;
+            while (sched.next(item, c0, c1)) {
+                int st = 0;                            // stages restart per segment
+                for (int c = c0; c < c1; ++c) {
                     const int b = q * S + st;
-                    if (C::kPerGroupIssuer && !C::kIssuerSpin) tc3::mbar_wait_sleep(&a_ready[b], (ph >> b) & 1u);
-                    else tc::mbar_wait(&a_ready[b], (ph >> b) & 1u);
-                    ph ^= 1u << b;
+                    tc3::mbar_wait_sleep(&a_ready[b], (ph >> st) & 1u);
+                    ph ^= 1u << st;
                     __syncwarp();
                     tc::fence_after();
                     tc3::issue_config(tmem_base + C::d_col(q, st), tmem_base + C::a_col(q, st),
                                       bq0, bq1, bq2, &d_ready[b]);
+                    st = st + 1 == S ? 0 : st + 1;
                 }
-                st = st + 1 == S ? 0 : st + 1;
             }
         }
     } else {
+        if (C::kMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 112;" ::: "memory");
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        uint32_t ta[S], td[S], ph[S], aph[S];
-        const uint32_t b_addr = tc::smem_u32(b_tile);
-        const uint64_t bq0 = tc2::slice_desc(b_addr), bq1 = tc2::slice_desc(b_addr + 1024),
-                       bq2 = tc2::slice_desc(b_addr + 2048);
-        const int wg = warp & 3;                  // warp within the group
+        uint32_t ta[S], td[S], ph[S];
 #pragma unroll
         for (int s2 = 0; s2 < S; ++s2) {
             ta[s2] = tmem_base + lane_off + C::a_col(g, s2);
             td[s2] = tmem_base + lane_off + C::d_col(g, s2);
             ph[s2] = 0;
-            aph[s2] = 0;
             tc2::tmem_st_zero4(ta[s2] + 20);      // never-written tail (columns 20-23)
         }
         tc2::tmem_st_wait();
@@ -315,12 +357,10 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
 #pragma unroll
         for (int l = 0; l < L; ++l) clamps[l] = 0;
         const int member = t & 1;
-        if (C::kStagger && g > 0) {
-            const long long t0 = clock64();
-            while (clock64() - t0 < (long long)g * 224) {}
-        }
 
-        for (int64_t blk = (int64_t)blockIdx.x * G + g; blk < nblocks; blk += total_groups) {
+        int64_t blk;
+        int cb, ce;
+        while (sched.next(blk, cb, ce)) {
             const int64_t pl = blk * tc::kPairsPerBlock + (t >> 1);
             const bool live = pl < a.P;
             int i = 0, j = 1;
@@ -381,79 +421,91 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     }
                 }
             };
-            auto load_d = [&](int s, float (&z)[HD + 2]) {
+            auto epilogue = [&](int c, int s) {
+                float z[HD + 2];
                 if (!C::kNoTensor) tc3::mbar_wait_warp(&dr[s], ph[s]);
                 ph[s] ^= 1u;
                 tc::fence_after();
                 tc::tmem_ld20(td[s], z);
-            };
-            auto epilogue = [&](int c, int s) {
-                float z[HD + 2];
-                load_d(s, z);
                 math(c, z);
             };
             auto build = [&](int c, int s) {
                 tc3::build_row(p2, krow + (uint32_t)c * (2 * ROW32 * 4), ta[s]);
-                if (C::kElected) {
-                    __syncwarp();
-                    if (lane == 0) tc2::mbar_arrive(&ar[s]);
-                } else {
-                    tc3::mbar_arrive_all(&ar[s]);
-                }
-                if (C::kComputeIssue) {
-                    if ((c & 3) == wg) {          // this warp's turn to issue config c
-                        tc::mbar_wait(&ar[s], aph[s]);
-                        __syncwarp();
-                        tc::fence_after();
-                        tc3::issue_config(tmem_base + C::d_col(g, s), tmem_base + C::a_col(g, s),
-                                          bq0, bq1, bq2, &dr[s]);
-                    }
-                    aph[s] ^= 1u;
-                }
+                __syncwarp();
+                if (lane == 0) tc2::mbar_arrive(&ar[s]);
                 asm volatile("" ::: "memory");   // keep build / epilogue phases apart
             };
 
-            if (C::kEarlyIssue) {
-                // pipeline: build(0 .. S-1); per c: D(c) -> registers, build(c+S)
-                // into the freed stage, then the math of c
-                auto step = [&](int cc, int s) {
-                    float z[HD + 2];
-                    load_d(s, z);
-                    if (cc + S < n_cfg) build(cc + S, s);
-                    math(cc, z);
-                };
-#pragma unroll
-                for (int u = 0; u < S; ++u)
-                    if (u < n_cfg) build(u, u);
-                int c0 = 0;                              // c0 % S == 0 throughout
-                for (; c0 + S <= n_cfg; c0 += S) {
-#pragma unroll
-                    for (int u = 0; u < S; ++u) step(c0 + u, u);
-                }
-#pragma unroll
-                for (int u = 0; u < S; ++u)
-                    if (c0 + u < n_cfg) step(c0 + u, u);
-            } else {
-            // software pipeline, stage of config c = c % S:
-            //   build(0 .. S-2); [build(c), epilogue(c-S+1)] for c >= S-1; drain
+            // software pipeline over this segment's configs [cb, ce), stage of
+            // config cb + u = u % S:
+            //   build(0 .. S-2); [build(u), epilogue(u-S+1)] for u >= S-1; drain
+            const int n = ce - cb;
 #pragma unroll
             for (int u = 0; u < S - 1; ++u)
-                if (u < n_cfg) build(u, u);
+                if (u < n) build(cb + u, u);
             int c = S - 1;                               // c % S == S - 1 throughout
-            for (; c + S <= n_cfg; c += S) {
+            for (; c + S <= n; c += S) {
 #pragma unroll
                 for (int u = 0; u < S; ++u) {
-                    build(c + u, (S - 1 + u) % S);
-                    epilogue(c + u - (S - 1), u % S);
+                    build(cb + c + u, (S - 1 + u) % S);
+                    epilogue(cb + c + u - (S - 1), u % S);
                 }
             }
 #pragma unroll
             for (int u = 0; u < 2 * S - 1; ++u) {
                 const int cc = c + u, x = cc - (S - 1);
-                if (cc < n_cfg) build(cc, (S - 1 + u) % S);
-                if (x >= 0 && x < n_cfg) epilogue(x, u % S);
+                if (cc < n) build(cb + cc, (S - 1 + u) % S);
+                if (x >= 0 && x < n) epilogue(cb + x, u % S);
             }
+
+            if (cb != 0 || ce != n_cfg) {
+                // ---- a piece of a split item: park it; the last piece merges ----
+                const uint32_t k = sched.k, item = (uint32_t)blk;
+                const int nf = 3 * L + 1;
+                float *mine = a.t.split_scratch +
+                              ((size_t)(k * 2 + sched.side(k, item)) * nf) * tc::kGroupThreads + t;
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    mine[(size_t)l * tc::kGroupThreads] = best[l];
+                    mine[(size_t)(L + l) * tc::kGroupThreads] = second[l];
+                    mine[(size_t)(2 * L + l) * tc::kGroupThreads] = __int_as_float(idx[l]);
+                }
+                mine[(size_t)(3 * L) * tc::kGroupThreads] = miny;
+                __threadfence();
+                tc3::group_sync(g);
+                const uint32_t kf = sched.slot_of(item * sched.n_cfg);
+                const uint32_t kl = sched.slot_of(item * sched.n_cfg + sched.n_cfg - 1);
+                if (t == 0) {
+                    const uint32_t old = atomicAdd(a.t.split_cnt + kf, 1u);
+                    const bool last = old == (uint32_t)(kl - kf);
+                    if (last) a.t.split_cnt[kf] = 0u;    // ready for the next launch
+                    s_last[g] = last;
+                }
+                tc3::group_sync(g);
+                if (!s_last[g]) continue;
+                __threadfence();
+                // merge the pieces in config order: first index of the minimum,
+                // runner-up = the smallest value that is not the winner
+#pragma unroll
+                for (int l = 0; l < L; ++l) { best[l] = FLT_MAX; second[l] = FLT_MAX; idx[l] = INT_MAX; }
+                miny = FLT_MAX;
+                for (uint32_t kk = kf; kk <= kl; ++kk) {
+                    const float *pc = a.t.split_scratch +
+                                      ((size_t)(kk * 2 + sched.side(kk, item)) * nf) * tc::kGroupThreads + t;
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        const float pb = __ldcg(pc + (size_t)l * tc::kGroupThreads);
+                        const float ps = __ldcg(pc + (size_t)(L + l) * tc::kGroupThreads);
+                        const int pi = __float_as_int(__ldcg(pc + (size_t)(2 * L + l) * tc::kGroupThreads));
+                        const bool lt = pb < best[l];
+                        second[l] = fminf(fminf(second[l], ps), lt ? best[l] : pb);
+                        idx[l] = lt ? pi : idx[l];
+                        best[l] = lt ? pb : best[l];
+                    }
+                    miny = fminf(miny, __ldcg(pc + (size_t)(3 * L) * tc::kGroupThreads));
+                }
             }
+
             // Floor clamps (estimator.py:106-109) are never counted from the
             // screen: a row whose screened predictions all lie above 0.5 + tau
             // has none, any other row is re-counted in fp64 by k_resolve
