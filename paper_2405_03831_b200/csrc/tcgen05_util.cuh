@@ -22,7 +22,7 @@ constexpr int kPairsPerBlock = 64;
 constexpr uint32_t kIdesc = (1u << 4)            // D = f32
                           | (0u << 7) | (0u << 10)  // A, B = f16
                           | (0u << 15) | (0u << 16) // both K-major
-                          | ((32u >> 3) << 17)      // N = 32
+                          | ((24u >> 3) << 17)      // N = 24: z2[0:18] + the head column
                           | ((128u >> 4) << 24);    // M = 128
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
