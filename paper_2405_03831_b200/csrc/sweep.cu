@@ -53,6 +53,7 @@ struct Net64P {          // 9.1 KB: needs the >4 KB kernel-parameter space (CUDA
     double wo[HD];
     double bo;
     double bounds[2 * NF];
+    double pad_;          // 16-B multiple: the image's w1t / w2t copies stay bulk-copyable
 };
 
 struct Net32P {          // fp32 screen: W2 as FFMA constant-bank operands
@@ -88,6 +89,7 @@ bool net64_from(const cs_network *net, Net64P *p) {
     memcpy(p->wo, net->w_out, sizeof(p->wo));
     p->bo = net->b_out[0];
     memcpy(p->bounds, net->feature_bounds, sizeof(p->bounds));
+    p->pad_ = 0.0;
     return true;
 }
 
@@ -211,7 +213,9 @@ __device__ __forceinline__ double head64t(const Head64P &net, const double *w2t,
 // Net64P.
 constexpr int kImgHeadOff = (HD * IN + HD);                  // doubles before Net64P::w2
 constexpr int kImgW1tOff = (int)(sizeof(Net64P) / 8);
-constexpr int kImgDoubles = kImgW1tOff + IN * HD;
+constexpr int kImgW2tOff = kImgW1tOff + IN * HD;              // w2 k-major (w2t[k][o])
+constexpr int kImgDoubles = kImgW2tOff + HD * HD;
+static_assert(sizeof(Net64P) % 16 == 0 && (IN * HD * 8) % 16 == 0, "bulk-copy granules");
 
 __device__ __forceinline__ const Head64P &stage_head64(const double *__restrict__ img, Head64P &sm) {
     const double *src = img + kImgHeadOff;
@@ -424,8 +428,8 @@ __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v >
 // bank serializes lane-divergent reads (lane h reading w1[h][k] is 18
 // different addresses), shared memory serves them in one wavefront; w1 is
 // also kept transposed (w1t[k][h]) so lane h's reads are consecutive.
-struct TablesSmem {
-    Net64P net;
+struct __align__(16) TablesSmem {
+    Net64P net;                  // net | w1t | head: one image slice + the head, bulk-copied
     double w1t[IN][HD];
     Head64P head;
     double xs[4][2 * NF];        // per warp: the app's normalized counters
@@ -471,18 +475,22 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
     // let a programmatically dependent sweep start its prologue now (it still
     // waits for this grid to finish before reading the tables)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    {
-        // coalesced copy of the device image (Net64P | w1t): the parameter
-        // bank would serialize these lane-divergent reads
-        const double *img = t.net_image;
-        double *dst = reinterpret_cast<double *>(&sm.net);
-        for (int i = threadIdx.x; i < kImgW1tOff; i += blockDim.x) dst[i] = __ldg(img + i);
-        double *w1t = &sm.w1t[0][0];
-        for (int i = threadIdx.x; i < IN * HD; i += blockDim.x) w1t[i] = __ldg(img + kImgW1tOff + i);
-        double *hd = reinterpret_cast<double *>(&sm.head);
-        for (int i = threadIdx.x; i < (int)(sizeof(Head64P) / 8); i += blockDim.x)
-            hd[i] = __ldg(img + kImgHeadOff + i);
+    // the device image (Net64P | w1t) and the head slice, staged by two TMA
+    // bulk copies (the parameter bank would serialize these lane-divergent
+    // reads; per-thread load/store loops left the block waiting on a chain of
+    // global-load latencies)
+    __shared__ uint64_t staged;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&staged, 1);
+        tc::fence_mbar_init();
+        constexpr uint32_t kNetW1t = (uint32_t)(sizeof(Net64P) + sizeof(double) * IN * HD);
+        static_assert(offsetof(TablesSmem, w1t) == sizeof(Net64P), "image order");
+        tc::mbar_expect_tx(&staged, kNetW1t + (uint32_t)sizeof(Head64P));
+        tc::bulk_g2s(&sm.net, t.net_image, kNetW1t, &staged);
+        tc::bulk_g2s(&sm.head, t.net_image + kImgHeadOff, (uint32_t)sizeof(Head64P), &staged);
     }
+    __syncthreads();
+    tc::mbar_wait(&staged, 0);
     // the image predates the previous kernel; the features may come from it
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // fresh counters for the screen (it reads them only after this grid completes)
@@ -736,10 +744,20 @@ __global__ void __launch_bounds__(128) k_resolve(const ResolveArgs a,
     __shared__ int red_i[4];
     // the weights do not depend on the screen: staged before the
     // programmatic-dependency wait (a no-op without a PDL launch)
+    // (the k-major W2 is a slice of the device image, like the head: two TMA
+    // bulk copies)
     __shared__ __align__(16) double w2t[HD * HD];
-    for (int q = threadIdx.x; q < HD * HD; q += blockDim.x)
-        w2t[q] = __ldg(a.t.net_image + kImgHeadOff + (q % HD) * HD + q / HD);
-    const Head64P &net64 = stage_head64(a.t.net_image, net_sm);   // (its __syncthreads covers w2t)
+    __shared__ uint64_t staged;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&staged, 1);
+        tc::fence_mbar_init();
+        tc::mbar_expect_tx(&staged, (uint32_t)(sizeof(w2t) + sizeof(Head64P)));
+        tc::bulk_g2s(w2t, a.t.net_image + kImgW2tOff, (uint32_t)sizeof(w2t), &staged);
+        tc::bulk_g2s(&net_sm, a.t.net_image + kImgHeadOff, (uint32_t)sizeof(Head64P), &staged);
+    }
+    __syncthreads();
+    tc::mbar_wait(&staged, 0);
+    const Head64P &net64 = net_sm;
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // blocks past both (device-side) queue lengths leave
     const uint32_t count = a.cnt->queue_len, rows = a.cnt->exact_rows;
@@ -1262,6 +1280,8 @@ int cs_tables_set_network(const cs_network *net, const cs_tables *tables, void *
     memcpy(img, &np, sizeof(Net64P));
     for (int h = 0; h < HD; ++h)
         for (int k = 0; k < IN; ++k) img[kImgW1tOff + k * HD + h] = np.w1[h * IN + k];
+    for (int o = 0; o < HD; ++o)
+        for (int k = 0; k < HD; ++k) img[kImgW2tOff + k * HD + o] = np.w2[o * HD + k];
     // pageable source: returns once the bytes are staged, so `img` may go out of scope
     if (cudaMemcpyAsync(tables->net_image, img, sizeof(img), cudaMemcpyHostToDevice,
                         (cudaStream_t)stream) != cudaSuccess) {
@@ -1606,7 +1626,8 @@ int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *
     // programmatic dependent launch behind the screen (see k_sweep_tc3)
     const Head64P h64 = head64_from(n64);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(sm_count() * 4));
+    // 2 blocks per SM at k_resolve's register count: one wave
+    cfg.gridDim = dim3((unsigned)(sm_count() * 2));
     cfg.blockDim = dim3(128);
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[1];
@@ -1616,7 +1637,7 @@ int resolve_impl(const cs_network *net, const cs_tables *tables, const cs_grid *
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, k_resolve, a, h64) != cudaSuccess) {
         cudaGetLastError();
-        k_resolve<<<sm_count() * 4, 128, 0, (cudaStream_t)stream>>>(a, h64);
+        k_resolve<<<sm_count() * 2, 128, 0, (cudaStream_t)stream>>>(a, h64);
     }
     return check_launch();
 }
