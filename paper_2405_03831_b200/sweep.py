@@ -9,6 +9,8 @@ is the 2-job special case; ``scheduler.build_graph`` wraps the result in a
 
 from __future__ import annotations
 
+import os
+
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -45,7 +47,7 @@ def plan_for(weights, spaces: Sequence[ConfigSpace], n: int, pair_begin: int = 0
     """A cached SweepPlan (buffers are reused across calls of the same shape)."""
     dev = require_cuda()
     key = (id(weights), tuple(spaces), n, pair_begin, pair_end, with_matrix, rel_eps, kernel,
-           str(dev))
+           str(dev), os.environ.get("COSCHED_TC_KIND"))
     with _CACHE_LOCK:
         hit = _PLAN_CACHE.get(key)
         if hit is not None and hit[0] is weights:

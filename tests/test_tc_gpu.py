@@ -65,3 +65,20 @@ def test_out_of_fp16_range_network_falls_back_and_stays_exact(weights):
     res = sweep_pairs(big, jobs, spaces, with_matrix=False)
     F, T = workload(n, 5)
     _check(res, oracle.sweep(big, F, T, KnobGrid(spaces)), 1)
+
+
+@pytest.mark.parametrize("kind", ["a03342", "3342"])
+@pytest.mark.parametrize("n,seed,budgets", [
+    (20, 0, (400.0,)), (131, 3, (400.0, 350.0)), (300, 4, (375.0,))])
+def test_alternative_screen_instances_match_oracle(weights, monkeypatch, kind, n, seed, budgets):
+    """The measured alternatives of k_sweep_tc3 stay parity-exact: the stream-K
+    schedule (0xA03342: items cut between group slots, merged by their last
+    piece -- at n=20 every item is split into several pieces) and the instance
+    without register rebalancing (0x3342)."""
+    monkeypatch.setenv("COSCHED_TC_KIND", kind)
+    spaces = [core.default_space(p) for p in budgets]
+    jobs = synth.generate_jobs(seed, synth.mixed_archetypes(n))
+    res = sweep_pairs(weights, jobs, spaces, with_matrix=False, kernel="tcgen05")
+    F, T = workload(n, seed)
+    ref = oracle.sweep(weights, F, T, KnobGrid(spaces))
+    _check(res, ref, len(spaces))
