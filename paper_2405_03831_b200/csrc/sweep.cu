@@ -2093,6 +2093,32 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
 }
 
 namespace {
+// A second stream (and events) per host thread for the chunked call below:
+// the D2H copies of finished row blocks run on it while the next chunk
+// computes.  Thread-local, so concurrent callers (and their graph captures)
+// never share a stream.
+constexpr int kMaxCallChunks = 16;
+struct CopyLane {
+    int device = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev[kMaxCallChunks + 1] = {};
+};
+CopyLane *copy_lane() {
+    thread_local CopyLane lane;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    if (lane.s && lane.device == dev) return &lane;
+    if (lane.s) {            // another device: the old lane's stream / events belong there
+        lane.s = nullptr;
+        for (auto &e : lane.ev) e = nullptr;
+    }
+    if (cudaStreamCreateWithFlags(&lane.s, cudaStreamNonBlocking) != cudaSuccess) { lane.s = nullptr; return nullptr; }
+    for (auto &e : lane.ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { lane.s = nullptr; return nullptr; }
+    lane.device = dev;
+    return &lane;
+}
+
 int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                        const double *h_base_time, int32_t n_apps, double rel_eps, char *ws,
                        const GraphLayout &L, double *h_weights, cs_pair_out h_pairs,
@@ -2133,18 +2159,79 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
                      stream));
     cs_pair_out po{(int32_t *)(ws + L.corun_idx), (double *)(ws + L.corun_time),
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
-    CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
-                              so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue),
-                              (cs_counters *)(ws + L.qcount), (unsigned long long *)(ws + L.clamps),
-                              h_weights ? (double *)(ws + L.W) : nullptr, CS_KERNEL_AUTO, stream));
-    if (h_weights)
-        CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
-                               cudaMemcpyDeviceToHost, st));
+    cs_counters *dcnt = (cs_counters *)(ws + L.qcount);
     const size_t LP = (size_t)nb * P, LN = (size_t)nb * n;
-    if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP, cudaMemcpyDeviceToHost, st));
-    if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));
-    if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen, po.corun_chosen, LP, cudaMemcpyDeviceToHost, st));
-    if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight, po.weight, 8 * LP, cudaMemcpyDeviceToHost, st));
+    // Large single-budget graphs: the pairs are swept in K chunks of whole
+    // matrix rows (rows [r_k, r_k+1) = the pairs (i, j) with r_k <= i < r_k+1,
+    // a contiguous pair range), and the host copies of a chunk's matrix rows
+    // and records run on a second stream while the next chunk computes.  Row
+    // block k is complete once chunks 0..k are: its upper part comes from
+    // chunk k, its lower part W[i][j < i] from the chunks of rows j.  The
+    // re-scan queue is per chunk (its counters are reset in between); the
+    // screen-error monitor, the sampled re-scan disagreements and the clamp
+    // counts accumulate over the chunks.
+    // (pinned destinations only: a pageable D2H would block the host thread
+    // and serialize the chunks)
+    CopyLane *lane = (nb == 1 && n_apps >= 1024 && mapped_v(h_weights) &&
+                      (!h_pairs.corun_grid_index || mapped_v(h_pairs.corun_grid_index)) &&
+                      (!h_pairs.corun_time || mapped_v(h_pairs.corun_time)) &&
+                      (!h_pairs.corun_chosen || mapped_v(h_pairs.corun_chosen)) &&
+                      (!h_pairs.weight || mapped_v(h_pairs.weight)))
+                         ? copy_lane() : nullptr;
+    if (lane) {
+        const int K = 8;
+        int64_t rows[K + 1];
+        rows[0] = 0;
+        rows[K] = n_apps;
+        for (int k = 1; k < K; ++k) {                  // equal pair counts per chunk
+            const int64_t target = P * k / K;
+            int64_t r = rows[k - 1];
+            while (r < n_apps - 1 && row_start(r + 1, n_apps) <= target) ++r;
+            rows[k] = r > rows[k - 1] ? r : rows[k - 1];
+        }
+        for (int k = 0; k < K; ++k) {
+            const int64_t r0 = rows[k], r1 = rows[k + 1];
+            if (r1 <= r0) continue;
+            const int64_t p0 = row_start(r0, n_apps), p1 = r1 >= n_apps - 1 ? P : row_start(r1, n_apps);
+            if (k > 0) {       // a fresh re-scan queue (its entries are chunk-relative)
+                CS_TRY(cudaMemsetAsync(&dcnt->queue_len, 0, sizeof(uint32_t), st));
+                CS_TRY(cudaMemsetAsync(&dcnt->exact_rows, 0, sizeof(uint32_t), st));
+            }
+            if (p1 > p0) {
+                cs_pair_out pk{po.corun_grid_index + p0, po.corun_time + p0, po.corun_chosen + p0,
+                               po.weight + p0};
+                CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
+                                          so.solo_clamps, p0, p1, rel_eps, pk, (int64_t *)(ws + L.queue),
+                                          dcnt, (unsigned long long *)(ws + L.clamps),
+                                          (double *)(ws + L.W), CS_KERNEL_AUTO, stream));
+            }
+            CS_TRY(cudaEventRecord(lane->ev[k], st));
+            CS_TRY(cudaStreamWaitEvent(lane->s, lane->ev[k], 0));
+            CS_TRY(cudaMemcpyAsync(h_weights + r0 * n, ws + L.W + sizeof(double) * r0 * n,
+                                   sizeof(double) * (r1 - r0) * n, cudaMemcpyDeviceToHost, lane->s));
+            const size_t np = (size_t)(p1 - p0);
+            if (np) {
+                if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index + p0, po.corun_grid_index + p0, 4 * np, cudaMemcpyDeviceToHost, lane->s));
+                if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time + p0, po.corun_time + p0, 8 * np, cudaMemcpyDeviceToHost, lane->s));
+                if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen + p0, po.corun_chosen + p0, np, cudaMemcpyDeviceToHost, lane->s));
+                if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight + p0, po.weight + p0, 8 * np, cudaMemcpyDeviceToHost, lane->s));
+            }
+        }
+        CS_TRY(cudaEventRecord(lane->ev[K], lane->s));     // join the copies back
+        CS_TRY(cudaStreamWaitEvent(st, lane->ev[K], 0));
+    } else {
+        CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
+                                  so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue), dcnt,
+                                  (unsigned long long *)(ws + L.clamps),
+                                  h_weights ? (double *)(ws + L.W) : nullptr, CS_KERNEL_AUTO, stream));
+        if (h_weights)
+            CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
+                                   cudaMemcpyDeviceToHost, st));
+        if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP, cudaMemcpyDeviceToHost, st));
+        if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));
+        if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen, po.corun_chosen, LP, cudaMemcpyDeviceToHost, st));
+        if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight, po.weight, 8 * LP, cudaMemcpyDeviceToHost, st));
+    }
     // small outputs (+ the queue length / screen-error monitor the caller
     // checks after the sync): one epilogue kernel when every destination is
     // pinned, else plain copies

@@ -165,3 +165,33 @@ def test_concurrent_decide_pair_equals_serial(weights):
         t.join()
     for o in outs:
         assert np.array_equal(o, ref)
+
+
+def test_chunked_host_call_overlaps_copies_and_stays_exact(weights):
+    """n >= 1,024, one budget, pinned host buffers: cs_build_graph_host sweeps
+    in row chunks and copies each finished row block + its records on a second
+    stream while the next chunk computes.  Eager, captured and replayed calls
+    (on a non-default stream) all equal the fp64 oracle bit for bit."""
+    from paper_2405_03831_b200.host_abi import HostGraphCall
+    n = 1100
+    F, T = workload(n, 11)
+    grid = KnobGrid([core.default_space(375.0)])
+    ref = oracle.sweep(weights, F, T, grid)
+    iu, ju = np.triu_indices(n, 1)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        call = HostGraphCall(weights, grid, n, with_records=True)
+        try:
+            for _ in range(4):                 # eager, eager, capture, replay
+                call.h_weights[...] = -1.0
+                call.h_idx[...] = -7
+                out = call(F, T)
+                W = out["weights"][0]
+                assert np.array_equal(W[iu, ju], ref["weight"][0])
+                assert np.array_equal(W[ju, iu], ref["weight"][0])
+                assert np.array_equal(call.h_idx[0], ref["corun_grid_index"][0])
+                assert np.array_equal(call.h_ct[0], ref["corun_time"][0])
+                assert np.array_equal(call.h_ch[0].astype(bool), ref["corun_chosen"][0])
+                assert np.array_equal(call.h_solo_time[0], ref["solo_time"][0])
+        finally:
+            call.close()
