@@ -92,6 +92,46 @@ class SweepResult:
         return (0.0 + st[i]) + st[j]
 
 
+class _PairWeights:
+    """(L, P) winning times read from the symmetric matrix on first use: with
+    the matrix on the host, copying the per-pair array as well would move the
+    same 8 bytes per pair over PCIe twice."""
+
+    def __init__(self, matrix: np.ndarray, n: int, pair_begin: int, pair_end: int):
+        self._m, self._n, self._b, self._e = matrix, n, pair_begin, pair_end
+        self._a = None
+
+    def _array(self) -> np.ndarray:
+        if self._a is None:
+            iu, ju = np.triu_indices(self._n, 1)
+            iu, ju = iu[self._b:self._e], ju[self._b:self._e]
+            self._a = np.stack([self._m[l][iu, ju] for l in range(self._m.shape[0])])
+        return self._a
+
+    def __getitem__(self, k):
+        return self._array()[k]
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._array()
+        return a if dtype is None else a.astype(dtype)
+
+    def __len__(self):
+        return self._m.shape[0]
+
+    @property
+    def shape(self):
+        return (self._m.shape[0], self._e - self._b)
+
+
+def _d2h(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> a fresh numpy array.  numpy advises huge pages for
+    large allocations, so the destination is not faulted in 4 KB at a time
+    (torch's .cpu() buffers are: ~2 GB/s for the 134 MB matrix at 4,096 apps)."""
+    out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
+    torch.from_numpy(out).copy_(t)
+    return out
+
+
 def _inputs(jobs: Sequence[JobProfile]):
     feats = np.stack([np.asarray(j.features, dtype=np.float64) for j in jobs])
     bt = np.array([float(j.base_time) for j in jobs], dtype=np.float64)
@@ -118,18 +158,19 @@ def run_plan(plan: SweepPlan, features: np.ndarray, base_time: np.ndarray,
                 plan.launch(d_f, d_b, rel_eps=eps)
                 c = plan.read_counters()
             P = plan.P
+            matrix = _d2h(plan.matrix) if (with_matrix and plan.matrix is not None) else None
             res = SweepResult(
                 n=plan.n, grid=plan.grid, pair_begin=plan.pair_begin, pair_end=plan.pair_end,
-                corun_grid_index=plan.corun_grid_index[:, :P].cpu().numpy(),
-                corun_time=plan.corun_time[:, :P].cpu().numpy(),
-                corun_chosen=plan.corun_chosen[:, :P].cpu().numpy().astype(bool),
-                weight=plan.weight[:, :P].cpu().numpy(),
-                solo_time=plan.solo_time.cpu().numpy(),
-                solo_split=plan.solo_split.cpu().numpy(),
-                solo_clamps=plan.solo_clamps.cpu().numpy(),
+                corun_grid_index=_d2h(plan.corun_grid_index[:, :P]),
+                corun_time=_d2h(plan.corun_time[:, :P]),
+                corun_chosen=_d2h(plan.corun_chosen[:, :P]).view(bool),
+                weight=(_PairWeights(matrix, plan.n, plan.pair_begin, plan.pair_end)
+                        if matrix is not None else _d2h(plan.weight[:, :P])),
+                solo_time=_d2h(plan.solo_time),
+                solo_split=_d2h(plan.solo_split),
+                solo_clamps=_d2h(plan.solo_clamps),
                 clamps=c.clamps, queue_len=c.queue_len, screen_error=c.screen_error,
-                exact_rows=c.exact_rows,
-                matrix=plan.matrix.cpu().numpy() if (with_matrix and plan.matrix is not None) else None)
+                exact_rows=c.exact_rows, matrix=matrix)
     if res.screen_error > 0.25 * eps or c.verify_fail:
         raise RuntimeError(f"fp32 screen error {res.screen_error:.3g} is too close to rel_eps "
                            f"{eps:.3g}; argmin parity is no longer guaranteed")
