@@ -1167,7 +1167,20 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
     // more than the idle SMs it fills); other 0xV3GS kinds select
     // the measured alternatives below and the timing-probe instances compiled
     // with -DCS_TIMING_PROBES (tools/build_probes.sh, never the product)
-    if (kind == CS_KERNEL_TCGEN05) kind = 0x203342;
+    if (kind == CS_KERNEL_TCGEN05) {
+        // Fewer work items than half the device's group slots (N <~ 180), or a
+        // few rounds whose last one is less than half full (N ~ 400-700): the
+        // stream-K schedule spreads the configs over every group slot
+        // (tools/time_steps.py: N=20 49 -> 32 us, N=128 58 -> 38 us, N=512
+        // 195 -> 181 us).  Otherwise whole items round-robin (at N=256 and
+        // N=4,096 the split items' refills and extra tails cost more than
+        // the idle slots they fill).
+        const int64_t slots = (int64_t)sm_count() * 4;
+        const int64_t rounds = (nblocks + slots - 1) / slots;
+        const bool few = 2 * nblocks <= slots;
+        const bool ragged = rounds >= 2 && rounds <= 8 && 2 * (nblocks - (rounds - 1) * slots) < slots;
+        kind = (few || ragged) ? 0xA03342 : 0x203342;
+    }
     const int G = (kind >> 4) & 0xF, S = kind & 0xF;
     int V = (kind >> 12) & 0xFFF;
     // stream-K keeps its schedule arithmetic in 32 bits
