@@ -82,3 +82,17 @@ def test_alternative_screen_instances_match_oracle(weights, monkeypatch, kind, n
     F, T = workload(n, seed)
     ref = oracle.sweep(weights, F, T, KnobGrid(spaces))
     _check(res, ref, len(spaces))
+
+
+@pytest.mark.parametrize("n,seed", [(3, 5), (40, 6)])
+def test_eight_budgets_small_n_stream_k(weights, n, seed):
+    """The most budgets a sweep takes (8, so the stream-K partials carry
+    3 x 8 + 1 fields per thread) on small N, where the screen splits the
+    configs of every work item across group slots."""
+    levels = (300, 325, 350, 375, 400, 425, 450, 475)
+    spaces = [core.ConfigSpace(p_total=float(p), cap_sum_levels=levels) for p in levels]
+    jobs = synth.generate_jobs(seed, synth.mixed_archetypes(n))
+    res = sweep_pairs(weights, jobs, spaces, with_matrix=True, kernel="tcgen05")
+    F, T = workload(n, seed)
+    ref = oracle.sweep(weights, F, T, KnobGrid(spaces))
+    _check(res, ref, len(spaces))
