@@ -1241,6 +1241,15 @@ extern "C" {
 
 const char *cs_version(void) { return "cosched_b200 0.1.0 (sm_100a)"; }
 
+#ifdef CS_TC_CLOCKS
+// DEBUG BUILDS ONLY: the screen's clock trace (tools/clock_trace.sh)
+int cs_debug_clocks(unsigned long long *h, int count) {
+    const int cap = (int)(sizeof(g_tc_clk) / sizeof(g_tc_clk[0]));
+    return cudaMemcpyFromSymbol(h, g_tc_clk, sizeof(unsigned long long) * (count < cap ? count : cap)) ==
+                   cudaSuccess ? 0 : CS_ERR_CUDA;
+}
+#endif
+
 const char *cs_error_string(int code) {
     switch (code) {
         case CS_OK: return "ok";

@@ -32,6 +32,14 @@
 // items round-robin.
 #pragma once
 
+#ifdef CS_TC_CLOCKS
+// DEBUG BUILDS ONLY (tools/clock_trace.sh): per-config timestamps of block 0's
+// first work item, configs [kClk0, kClk0 + 32), read back by cs_debug_clocks
+__device__ unsigned long long g_tc_clk[4 * 4 * 4 * 32 + 4 * 2 * 32];
+constexpr int kClk0 = 20;
+#define TC_CLK(slot) (g_tc_clk[slot] = clock64())
+#endif
+
 namespace tc3 {
 
 // V bit 0: one elected arrive per warp on a_ready (count 4);
@@ -330,11 +338,19 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                 for (int c = c0; c < c1; ++c) {
                     const int b = q * S + st;
                     tc3::mbar_wait_sleep(&a_ready[b], (ph >> st) & 1u);
+#ifdef CS_TC_CLOCKS
+                    const bool clk = blockIdx.x == 0 && item == (int64_t)q && lane == 0 &&
+                                     c >= kClk0 && c < kClk0 + 32;
+                    if (clk) TC_CLK(4 * 4 * 4 * 32 + (q * 2 + 0) * 32 + (c - kClk0));
+#endif
                     ph ^= 1u << st;
                     __syncwarp();
                     tc::fence_after();
                     tc3::issue_config(tmem_base + C::d_col(q, st), tmem_base + C::a_col(q, st),
                                       bq0, bq1, bq2, &d_ready[b]);
+#ifdef CS_TC_CLOCKS
+                    if (clk) TC_CLK(4 * 4 * 4 * 32 + (q * 2 + 1) * 32 + (c - kClk0));
+#endif
                     st = st + 1 == S ? 0 : st + 1;
                 }
             }
@@ -421,18 +437,37 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     }
                 }
             };
+#ifdef CS_TC_CLOCKS
+            const bool clk_item = blockIdx.x == 0 && blk == (int64_t)g && lane == 0;
+            auto clk_at = [&](int c, int ev) {
+                if (clk_item && c >= kClk0 && c < kClk0 + 32)
+                    TC_CLK(((g * 4 + (warp & 3)) * 4 + ev) * 32 + (c - kClk0));
+            };
+#endif
             auto epilogue = [&](int c, int s) {
                 float z[HD + 2];
+#ifdef CS_TC_CLOCKS
+                clk_at(c, 2);
+#endif
                 if (!C::kNoTensor) tc3::mbar_wait_warp(&dr[s], ph[s]);
+#ifdef CS_TC_CLOCKS
+                clk_at(c, 3);
+#endif
                 ph[s] ^= 1u;
                 tc::fence_after();
                 tc::tmem_ld20(td[s], z);
                 math(c, z);
             };
             auto build = [&](int c, int s) {
+#ifdef CS_TC_CLOCKS
+                clk_at(c, 0);
+#endif
                 tc3::build_row(p2, krow + (uint32_t)c * (2 * ROW32 * 4), ta[s]);
                 __syncwarp();
                 if (lane == 0) tc2::mbar_arrive(&ar[s]);
+#ifdef CS_TC_CLOCKS
+                clk_at(c, 1);
+#endif
                 asm volatile("" ::: "memory");   // keep build / epilogue phases apart
             };
 
