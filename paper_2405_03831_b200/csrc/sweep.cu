@@ -370,17 +370,6 @@ __device__ __forceinline__ void write_winner(const SweepArgs &a, int l, int64_t 
     a.out.corun_time[o] = co;
     monitor(a, co, best);
 }
-// the same without the monitor: the caller reduces screen_gap_bits over its
-// warp first (one atomic per warp instead of one per pair on one address)
-__device__ __forceinline__ void write_winner_only(const SweepArgs &a, int l, int64_t pl, int idx,
-                                                  double co) {
-    const int64_t o = (int64_t)l * a.P + pl;
-    a.out.corun_grid_index[o] = idx;
-    a.out.corun_time[o] = co;
-}
-__device__ __forceinline__ uint32_t screen_gap_bits(double exact, float screened) {
-    return __float_as_uint((float)(fabs(exact - (double)screened) / exact));
-}
 
 // co-run vs time-share for one (pair, budget) (hwopt.py:77-87) with the solo
 // pair sum (0.0 + t_i) + t_j (estimator.py:168-178); writes the flag and the

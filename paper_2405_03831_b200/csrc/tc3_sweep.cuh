@@ -555,19 +555,15 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     : C::kNoExact ? (double)best[l]
                     : member_time64_lean(a.t, *net64, a.base_time, self, other, idx[l], member);
                 const double co = fmax(tm64, __shfl_xor_sync(0xffffffffu, tm64, 1));
-                uint32_t gap = 0;             // the screen-error monitor, warp-reduced below
                 if (live && member == 0 && !C::kNoWrite) {
                     if (ambiguous) {
                         push_ambiguous(a, l, pl);
                     } else {
-                        write_winner_only(a, l, pl, idx[l], co);
-                        gap = screen_gap_bits(co, best[l]);
+                        write_winner(a, l, pl, idx[l], co, best[l]);
                         maybe_verify(a, l, pl, best[l], second[l]);
                         if (a.fused) clamps[l] += decide_write(a, l, pl, i, j, idx[l], co);
                     }
                 }
-                gap = __reduce_max_sync(0xffffffffu, gap);
-                if (lane == 0 && gap) atomicMax(&a.cnt->screen_err_bits, gap);
             }
         }
 #pragma unroll
