@@ -2058,6 +2058,9 @@ int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const doub
         if (state) state->key.clear();   // the workspace contents are unknown now
         return code;
     };
+    static const bool dbg = getenv("CS_DEBUG_HOSTCALL") != nullptr;
+    if (dbg) fprintf(stderr, "cs_build_graph_host: %s (capturable %d)\n",
+                     exec ? "graph replay" : try_capture ? "capture" : "eager", (int)capturable);
     if (exec) {
         if (cudaGraphLaunch(exec, st) != cudaSuccess) { cudaGetLastError(); return fail(CS_ERR_CUDA); }
     } else if (try_capture) {
