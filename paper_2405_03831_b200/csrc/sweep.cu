@@ -1216,6 +1216,7 @@ int launch_sweep(const SweepArgs &a, const Net32P &net, const Head64P &h64, int 
     CS_TC3(4, 2, 3)      // round-robin, no register rebalancing
 #ifdef CS_TIMING_PROBES
     CS_TC3(4, 2, 531) CS_TC3(4, 2, 579) CS_TC3(4, 2, 595)
+    CS_TC3(4, 2, 1539)   // single-term screen (bit 10)
 #endif
 #undef CS_TC3
     return CS_ERR_ARG;

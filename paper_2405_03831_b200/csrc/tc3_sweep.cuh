@@ -45,6 +45,8 @@ namespace tc3 {
 // V bit 0: one elected arrive per warp on a_ready (count 4);
 // V bit 1: one MMA-issuer warp per group;
 // V bit 9: setmaxnreg register rebalancing (issuers 32, compute 112);
+// V bit 10: single-term screen -- A = fp16 RN(ReLU(z1)) only (no lo split),
+//           3 MMAs (A W2hi + A W2lo + tail); needs a wider ambiguity band;
 // V bit 11: stream-K work schedule (above).
 // Timing probes (tools/build_probes.sh, -DCS_TIMING_PROBES; WRONG results by
 // design, never in the product .so): bit 4 no MMAs / waits, bit 6 no fp64
@@ -53,6 +55,7 @@ template <int G, int S, int V = 0>
 struct Cfg {
     static constexpr bool kMaxNReg = (V & 512) != 0;
     static constexpr bool kStreamK = (V & 2048) != 0;
+    static constexpr bool kOneTerm = (V & 1024) != 0;
 #ifdef CS_TIMING_PROBES
     static constexpr bool kNoTensor = (V & 16) != 0;
     static constexpr bool kNoExact = (V & 64) != 0;
@@ -125,8 +128,25 @@ __device__ __forceinline__ void tmem_st20_848(uint32_t taddr, const uint32_t (&w
 // this way against 75+ for a `lane == 0` branch (the tensor pipe itself
 // sustains one M128 N32 K16 MMA per ~16 cycles per SM).
 //   z2 = A_s0 q0 + A_s1 q0 + A_s2 q1 + A_s0 q2
+template <bool kOneTerm>
 __device__ __forceinline__ void issue_config(uint32_t d_t, uint32_t a_t, uint64_t bq0, uint64_t bq1,
                                              uint64_t bq2, uint64_t *bar) {
+    if constexpr (kOneTerm) {
+        // z2 = A_s0 q0 + A_s2 q1 + A_s0 q2 (A_s2 column 17 holds zeros)
+        asm volatile(
+            "{\n\t.reg .pred e, pf, pt;\n\t"
+            "setp.ne.b32 pf, %6, %6;\n\t"
+            "setp.eq.b32 pt, %6, %6;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %6, pf;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %4, %6, pt;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %6, pt;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%2];\n}"
+            ::"r"(d_t), "r"(a_t), "r"(tc::smem_u32(bar)), "l"(bq0), "l"(bq1), "l"(bq2), "r"(tc::kIdesc),
+              "r"(a_t + 16)
+            : "memory");
+        return;
+    }
     asm volatile(
         "{\n\t.reg .pred e, pf, pt;\n\t"
         "setp.ne.b32 pf, %6, %6;\n\t"
@@ -157,6 +177,7 @@ __device__ __forceinline__ float2 lds2(uint32_t a) {
 // tcgen05_util.cuh), stored into its TMEM lane.  krow: 32-bit shared-window
 // address of this member's K row (a plain integer, so ptxas never re-derives
 // the generic->shared mapping in the loop)
+template <bool kOneTerm>
 __device__ __forceinline__ void build_row(const float2 (&p2)[9], uint32_t krow, uint32_t taddr) {
     const float4 q0 = lds4(krow), q1 = lds4(krow + 16), q2 = lds4(krow + 32), q3 = lds4(krow + 48);
     const float2 q4 = lds2(krow + 64);
@@ -165,6 +186,25 @@ __device__ __forceinline__ void build_row(const float2 (&p2)[9], uint32_t krow, 
                           make_float2(q2.x, q2.y), make_float2(q2.z, q2.w),
                           make_float2(q3.x, q3.y), make_float2(q3.z, q3.w), q4};
     uint32_t w[20];
+    if constexpr (kOneTerm) {
+        // hi only, rounded to nearest; columns 8-15 are never read
+#pragma unroll
+        for (int v = 0; v < 9; ++v) {
+            const float2 z = tc2::add2(p2[v], kr[v]);
+            const uint32_t hw = tc2::cvt_rn_relu(z.x, z.y);
+            if (v < 8) w[v] = hw;
+            else w[16] = hw;
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + 16),
+                     "r"(w[16]), "r"(0u), "r"(0x3C003C00u), "r"(w[16])
+                     : "memory");
+        tc2::tmem_st_wait();
+        tc::fence_before();
+        return;
+    }
 #pragma unroll
     for (int v = 0; v < 9; ++v) {
         const float2 z = tc2::add2(p2[v], kr[v]);
@@ -346,7 +386,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
                     ph ^= 1u << st;
                     __syncwarp();
                     tc::fence_after();
-                    tc3::issue_config(tmem_base + C::d_col(q, st), tmem_base + C::a_col(q, st),
+                    tc3::issue_config<C::kOneTerm>(tmem_base + C::d_col(q, st), tmem_base + C::a_col(q, st),
                                       bq0, bq1, bq2, &d_ready[b]);
 #ifdef CS_TC_CLOCKS
                     if (clk) TC_CLK(4 * 4 * 4 * 32 + (q * 2 + 1) * 32 + (c - kClk0));
@@ -462,7 +502,7 @@ __global__ void __launch_bounds__(tc3::Cfg<G, S, V>::kThreads, 1)
 #ifdef CS_TC_CLOCKS
                 clk_at(c, 0);
 #endif
-                tc3::build_row(p2, krow + (uint32_t)c * (2 * ROW32 * 4), ta[s]);
+                tc3::build_row<C::kOneTerm>(p2, krow + (uint32_t)c * (2 * ROW32 * 4), ta[s]);
                 __syncwarp();
                 if (lane == 0) tc2::mbar_arrive(&ar[s]);
 #ifdef CS_TC_CLOCKS
