@@ -326,7 +326,11 @@ int cs_workspace_release(void *d_workspace);
 /* h_weights: L x N x N (NULL to skip); h_pairs members: L x P host arrays
  * (NULL members skipped); h_solo members: L x N host arrays (NULL skipped);
  * h_clamps: L (NULL to skip).  Full graph (all P pairs).  Synchronizes
- * `stream` before returning. */
+ * `stream` before returning.  Transfers: pinned inputs are read by a
+ * zero-copy kernel; when every destination is pinned, ONE epilogue kernel
+ * writes all outputs into them over PCIe (else cudaMemcpyAsync per array);
+ * single-budget calls with >= 14 MB of pinned outputs sweep in 8 row chunks
+ * and copy each finished row block while the next one computes. */
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                         const double *h_base_time, int32_t n_apps, double rel_eps,
                         void *d_workspace, size_t workspace_bytes, double *h_weights,

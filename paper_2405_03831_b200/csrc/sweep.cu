@@ -1831,29 +1831,35 @@ __global__ void k_call_begin(const double *__restrict__ hf, const double *__rest
     }
 }
 
-// Host-call epilogue: the small outputs straight into pinned host memory
-// (one launch instead of up to five D2H copies).  Null destinations skipped.
+// Host-call epilogue: every output straight into pinned host memory -- the
+// N x N matrix, the per-pair records, the solo results, the clamp counts and
+// the counters -- by one launch of coalesced 16-byte stores over PCIe instead
+// of up to eleven D2H copies (each a DMA setup on the call's critical path).
+// Segments whose ends are not 16-byte aligned are copied bytewise.
+constexpr int kCallSegs = 12;
 struct CallEndArgs {
-    const double *solo_time;
-    const int32_t *solo_split, *solo_clamps;
-    const unsigned long long *clamps;
-    const uint32_t *counters;
-    double *h_solo_time;
-    int32_t *h_solo_split, *h_solo_clamps;
-    unsigned long long *h_clamps;
-    uint32_t *h_counters;
-    int64_t LN;
-    int nb;
+    const uint8_t *src[kCallSegs];
+    uint8_t *dst[kCallSegs];
+    int64_t bytes[kCallSegs];
+    int64_t start16[kCallSegs + 1];   // prefix sums of the segments' 16-byte chunks
+    uint32_t aligned;                 // bit g: segment g's src and dst are 16-byte aligned
+    int n;
 };
 __global__ void k_call_end(const CallEndArgs a) {
-    const int64_t total = 3 * a.LN + a.nb + 4;
+    const int64_t total = a.start16[a.n];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
-        if (k < a.LN) { if (a.h_solo_time) a.h_solo_time[k] = a.solo_time[k]; }
-        else if (k < 2 * a.LN) { if (a.h_solo_split) a.h_solo_split[k - a.LN] = a.solo_split[k - a.LN]; }
-        else if (k < 3 * a.LN) { if (a.h_solo_clamps) a.h_solo_clamps[k - 2 * a.LN] = a.solo_clamps[k - 2 * a.LN]; }
-        else if (k < 3 * a.LN + a.nb) { if (a.h_clamps) a.h_clamps[k - 3 * a.LN] = a.clamps[k - 3 * a.LN]; }
-        else a.h_counters[k - 3 * a.LN - a.nb] = a.counters[k - 3 * a.LN - a.nb];
+        int g = 0;
+        while (k >= a.start16[g + 1]) ++g;
+        const int64_t off = (k - a.start16[g]) * 16;
+        const int64_t rem = a.bytes[g] - off;
+        if (rem >= 16 && ((a.aligned >> g) & 1u)) {
+            *reinterpret_cast<uint4 *>(a.dst[g] + off) =
+                __ldcg(reinterpret_cast<const uint4 *>(a.src[g] + off));
+        } else {
+            const int m = rem < 16 ? (int)rem : 16;
+            for (int b = 0; b < m; ++b) a.dst[g][off + b] = a.src[g][off + b];
+        }
     }
 }
 
@@ -2198,7 +2204,16 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     // counts accumulate over the chunks.
     // (pinned destinations only: a pageable D2H would block the host thread
     // and serialize the chunks)
-    CopyLane *lane = (nb == 1 && n_apps >= 1024 && mapped_v(h_weights) &&
+    // Chunking pays once the D2H bytes outweigh its fixed cost (8 launches,
+    // ragged rounds): measured crossover ~14 MB (N ~ 1,000 with records,
+    // ~1,400 without; tools/e2e_breakdown.py).  Below it the single sweep and
+    // the one-kernel zero-copy epilogue win.
+    static const double min_chunk_bytes =
+        getenv("CS_HOSTCALL_CHUNK_BYTES") ? atof(getenv("CS_HOSTCALL_CHUNK_BYTES")) : 14e6;
+    const double d2h_bytes = (h_weights ? 8.0 * n * n * nb : 0.0) +
+                             (double)LP * ((h_pairs.corun_grid_index ? 4 : 0) + (h_pairs.corun_time ? 8 : 0) +
+                                           (h_pairs.corun_chosen ? 1 : 0) + (h_pairs.weight ? 8 : 0));
+    CopyLane *lane = (nb == 1 && d2h_bytes >= min_chunk_bytes && mapped_v(h_weights) &&
                       (!h_pairs.corun_grid_index || mapped_v(h_pairs.corun_grid_index)) &&
                       (!h_pairs.corun_time || mapped_v(h_pairs.corun_time)) &&
                       (!h_pairs.corun_chosen || mapped_v(h_pairs.corun_chosen)) &&
@@ -2250,32 +2265,52 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
                                   so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue), dcnt,
                                   (unsigned long long *)(ws + L.clamps),
                                   h_weights ? (double *)(ws + L.W) : nullptr, CS_KERNEL_AUTO, stream));
-        if (h_weights)
-            CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
-                                   cudaMemcpyDeviceToHost, st));
-        if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP, cudaMemcpyDeviceToHost, st));
-        if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));
-        if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen, po.corun_chosen, LP, cudaMemcpyDeviceToHost, st));
-        if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight, po.weight, 8 * LP, cudaMemcpyDeviceToHost, st));
     }
-    // small outputs (+ the queue length / screen-error monitor the caller
-    // checks after the sync): one epilogue kernel when every destination is
-    // pinned, else plain copies
-    CallEndArgs e{so.solo_time, so.solo_split, so.solo_clamps,
-                  (const unsigned long long *)(ws + L.clamps), (const uint32_t *)(ws + L.qcount),
-                  (double *)mapped_v(h_solo.solo_time), (int32_t *)mapped_v(h_solo.solo_split),
-                  (int32_t *)mapped_v(h_solo.solo_clamps), (unsigned long long *)mapped_v(h_clamps),
-                  (uint32_t *)mapped_v(h_counters), (int64_t)LN, nb};
-    const bool zc_out = e.h_counters && (!h_solo.solo_time || e.h_solo_time) &&
-                        (!h_solo.solo_split || e.h_solo_split) &&
-                        (!h_solo.solo_clamps || e.h_solo_clamps) && (!h_clamps || e.h_clamps);
+    // the outputs (+ the queue length / screen-error monitor the caller checks
+    // after the sync): one epilogue kernel when every destination is pinned,
+    // else plain copies
+    CallEndArgs e{};
+    bool zc_out = true;
+    auto seg = [&](void *h_dst, const void *d_src, size_t bytes) {
+        if (!h_dst || !bytes || !zc_out) return;
+        void *m = mapped_v(h_dst);
+        if (!m || e.n == kCallSegs) { zc_out = false; return; }
+        e.src[e.n] = (const uint8_t *)d_src;
+        e.dst[e.n] = (uint8_t *)m;
+        e.bytes[e.n] = (int64_t)bytes;
+        if ((((uintptr_t)d_src | (uintptr_t)m) & 15) == 0) e.aligned |= 1u << e.n;
+        e.start16[e.n + 1] = e.start16[e.n] + (int64_t)((bytes + 15) / 16);
+        ++e.n;
+    };
+    if (!lane) {
+        if (h_weights) seg(h_weights, ws + L.W, sizeof(double) * n * n * nb);
+        seg(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP);
+        seg(h_pairs.corun_time, po.corun_time, 8 * LP);
+        seg(h_pairs.corun_chosen, po.corun_chosen, LP);
+        seg(h_pairs.weight, po.weight, 8 * LP);
+    }
+    seg(h_solo.solo_time, so.solo_time, 8 * LN);
+    seg(h_solo.solo_split, so.solo_split, 4 * LN);
+    seg(h_solo.solo_clamps, so.solo_clamps, 4 * LN);
+    seg(h_clamps, ws + L.clamps, 8 * (size_t)nb);
+    seg(h_counters, ws + L.qcount, sizeof(cs_counters));
     if (zc_out) {
-        const int64_t items = 3 * (int64_t)LN + nb + 4;
+        const int64_t items = e.start16[e.n];
         int blocks = (int)((items + 255) / 256);
-        if (blocks > sm_count()) blocks = sm_count();
+        if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
+        if (blocks < 1) blocks = 1;
         k_call_end<<<blocks, 256, 0, st>>>(e);
         CS_TRY(cudaGetLastError());
     } else {
+        if (!lane) {
+            if (h_weights)
+                CS_TRY(cudaMemcpyAsync(h_weights, ws + L.W, sizeof(double) * n * n * nb,
+                                       cudaMemcpyDeviceToHost, st));
+            if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP, cudaMemcpyDeviceToHost, st));
+            if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time, po.corun_time, 8 * LP, cudaMemcpyDeviceToHost, st));
+            if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen, po.corun_chosen, LP, cudaMemcpyDeviceToHost, st));
+            if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight, po.weight, 8 * LP, cudaMemcpyDeviceToHost, st));
+        }
         if (h_solo.solo_time) CS_TRY(cudaMemcpyAsync(h_solo.solo_time, so.solo_time, 8 * LN, cudaMemcpyDeviceToHost, st));
         if (h_solo.solo_split) CS_TRY(cudaMemcpyAsync(h_solo.solo_split, so.solo_split, 4 * LN, cudaMemcpyDeviceToHost, st));
         if (h_solo.solo_clamps) CS_TRY(cudaMemcpyAsync(h_solo.solo_clamps, so.solo_clamps, 4 * LN, cudaMemcpyDeviceToHost, st));

@@ -97,12 +97,15 @@ class HostGraphCall:
         self._t_cl, h_cl = _pinned((L,), torch.int64)
         self.h_clamps = h_cl.view(np.uint64)
         self.h_clamps[...] = 0
-        self._stream = torch.cuda.current_stream(self.device).cuda_stream
+        # a private non-default stream: the call is synchronous (it returns
+        # after its results sit in the host buffers), and the library captures
+        # a repeated call on a non-default stream into a CUDA graph
+        self._stream_obj = torch.cuda.Stream(self.device)
         self._net_obj = self.net
         self._args = (self.net.ref(), ctypes.byref(self.cgrid), nat.ptr(self.h_features),
                       nat.ptr(self.h_base_time), self.n, self.rel_eps, self.ws_ptr, self.ws_bytes,
                       nat.ptr(self.h_weights), self.pairs, self.solo,
-                      self.h_clamps.ctypes.data_as(nat.c_ull_p))
+                      self.h_clamps.ctypes.data_as(nat.c_ull_p), self._stream_obj.cuda_stream)
 
     def close(self) -> None:
         """Drop the workspace's library-side state (before its memory goes)."""
@@ -133,11 +136,10 @@ class HostGraphCall:
             self.h_features[...] = features
         if base_time is not None:
             self.h_base_time[...] = base_time
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        if self.net is not self._net_obj or stream != self._stream:
-            self._stream, self._net_obj = stream, self.net
+        if self.net is not self._net_obj:
+            self._net_obj = self.net
             self._args = (self.net.ref(),) + self._args[1:]
-        rc = self.lib.cs_build_graph_host(*self._args, stream)
+        rc = self.lib.cs_build_graph_host(*self._args)
         nat.check(rc, "cs_build_graph_host")
         out = {"weights": self.h_weights, "solo_time": self.h_solo_time,
                "solo_split": self.h_solo_split, "solo_clamps": self.h_solo_clamps,

@@ -168,7 +168,7 @@ def test_concurrent_decide_pair_equals_serial(weights):
 
 
 def test_chunked_host_call_overlaps_copies_and_stays_exact(weights):
-    """n >= 1,024, one budget, pinned host buffers: cs_build_graph_host sweeps
+    """~18 MB of pinned D2H (n = 1,100, one budget, records): cs_build_graph_host sweeps
     in row chunks and copies each finished row block + its records on a second
     stream while the next chunk computes.  Eager, captured and replayed calls
     (on a non-default stream) all equal the fp64 oracle bit for bit."""
@@ -195,3 +195,52 @@ def test_chunked_host_call_overlaps_copies_and_stays_exact(weights):
                 assert np.array_equal(call.h_solo_time[0], ref["solo_time"][0])
         finally:
             call.close()
+
+
+def test_zero_copy_epilogue_with_misaligned_pinned_outputs(weights):
+    """Every destination pinned but the record arrays placed at odd offsets
+    inside one pinned buffer: the one-kernel epilogue (16-byte stores where
+    both ends are aligned, bytewise otherwise) still delivers every output
+    exactly; repeated calls on a non-default stream replay a captured graph."""
+    lib = nat.sweep_lib()
+    n = 130
+    F, T = workload(n, 5)
+    grid = KnobGrid([core.default_space(400.0)])
+    cgrid, keep = _host_grid(grid)
+    net = NetworkABI(weights)
+    P = n * (n - 1) // 2
+    nbytes = lib.cs_build_graph_workspace_bytes(n, ctypes.byref(cgrid))
+    ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+    ws_ptr = (ws.data_ptr() + 255) & ~255
+    nat.check(lib.cs_workspace_retain(ws_ptr, nbytes), "retain")
+    iu, ju, ref = _expected(weights, F, T, grid, n)
+    pin = lambda nb: torch.empty(nb, dtype=torch.uint8, pin_memory=True).numpy()
+    raw = pin(8 * P + 4 * P + P + 64)
+    idx = raw[1:1 + 4 * P].view(np.int32)            # odd offsets: bytewise path
+    ct = raw[4 * P + 3:4 * P + 3 + 8 * P].view(np.float64)
+    ch = raw[12 * P + 5:12 * P + 5 + P]
+    hf = pin(F.nbytes).view(np.float64).reshape(F.shape); hf[...] = F
+    hb = pin(T.nbytes).view(np.float64); hb[...] = T
+    W = pin(8 * n * n).view(np.float64).reshape(1, n, n)
+    st = pin(8 * n).view(np.float64)
+    ss = pin(4 * n).view(np.int32)
+    cl = pin(8).view(np.uint64)
+    s = torch.cuda.Stream()
+    try:
+        for _ in range(4):                       # eager, eager, capture, replay
+            W[...] = -1.0; idx[...] = -9; ct[...] = 0.0; ch[...] = 7
+            rc = lib.cs_build_graph_host(net.ref(), ctypes.byref(cgrid), nat.ptr(hf), nat.ptr(hb), n,
+                                         1e-5, ws_ptr, nbytes, nat.ptr(W),
+                                         nat.CsPairOut(nat.ptr(idx, nat.c_int32_p), nat.ptr(ct),
+                                                       nat.ptr(ch, nat.c_uint8_p), None),
+                                         nat.CsSoloOut(nat.ptr(st), nat.ptr(ss, nat.c_int32_p), None),
+                                         cl.ctypes.data_as(nat.c_ull_p), s.cuda_stream)
+            nat.check(rc, "cs_build_graph_host")
+            assert np.array_equal(W[0][iu, ju], ref["weight"][0])
+            assert np.array_equal(W[0][ju, iu], ref["weight"][0])
+            assert np.array_equal(idx, ref["corun_grid_index"][0])
+            assert np.array_equal(ct, ref["corun_time"][0])
+            assert np.array_equal(ch.astype(bool), ref["corun_chosen"][0])
+            assert np.array_equal(st, ref["solo_time"][0])
+    finally:
+        lib.cs_workspace_release(ws_ptr)

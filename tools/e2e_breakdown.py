@@ -48,3 +48,32 @@ rawmin = lambda: lib.cs_build_graph_host(*args_min)
 print(f"  raw, no D2H at all but counters: median {wall(rawmin)[0]:.1f} us", flush=True)
 # device-only reference: the same work as a plain stream-ordered launch + sync
 torch.cuda.synchronize()
+from paper_2405_03831_b200.device import SweepPlan, to_device_inputs
+plan = SweepPlan(w, grid, n, with_matrix=True)
+d_f, d_b = to_device_inputs(F, T, plan.device)
+side = torch.cuda.Stream()
+side.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(side):
+    plan.launch(d_f, d_b)
+torch.cuda.current_stream().wait_stream(side)
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    plan.launch(d_f, d_b)
+def dev_only():
+    g.replay()
+    torch.cuda.synchronize()
+print(f"  device-only graph replay + sync (no copies): median {wall(dev_only)[0]:.1f} us", flush=True)
+e = torch.cuda.CUDAGraph()
+tiny = torch.zeros(1, device=plan.device)
+with torch.cuda.graph(e):
+    tiny.add_(1)
+def empty():
+    e.replay()
+    torch.cuda.synchronize()
+print(f"  one-kernel graph replay + sync: median {wall(empty)[0]:.1f} us", flush=True)
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+acc = []
+for _ in range(200):
+    ev0.record(); g.replay(); ev1.record(); ev1.synchronize(); acc.append(ev0.elapsed_time(ev1) * 1e3)
+print(f"  device-only graph, event-timed: median {float(np.median(acc)):.1f} us", flush=True)
