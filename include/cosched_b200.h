@@ -329,7 +329,7 @@ int cs_workspace_release(void *d_workspace);
  * `stream` before returning.  Transfers: pinned inputs are read by a
  * zero-copy kernel; when every destination is pinned, ONE epilogue kernel
  * writes all outputs into them over PCIe (else cudaMemcpyAsync per array);
- * single-budget calls with >= 14 MB of pinned outputs sweep in 8 row chunks
+ * calls with >= 14 MB of pinned outputs sweep in 8 row chunks
  * and copy each finished row block while the next one computes. */
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
                         const double *h_base_time, int32_t n_apps, double rel_eps,

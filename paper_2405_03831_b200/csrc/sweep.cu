@@ -2193,7 +2193,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
                    (uint8_t *)(ws + L.chosen), (double *)(ws + L.weight)};
     cs_counters *dcnt = (cs_counters *)(ws + L.qcount);
     const size_t LP = (size_t)nb * P, LN = (size_t)nb * n;
-    // Large single-budget graphs: the pairs are swept in K chunks of whole
+    // Large graphs: the pairs are swept in K chunks of whole
     // matrix rows (rows [r_k, r_k+1) = the pairs (i, j) with r_k <= i < r_k+1,
     // a contiguous pair range), and the host copies of what a chunk made final
     // (its rows' upper part and its columns' lower part) and of its records
@@ -2212,7 +2212,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     const double d2h_bytes = (h_weights ? 8.0 * n * n * nb : 0.0) +
                              (double)LP * ((h_pairs.corun_grid_index ? 4 : 0) + (h_pairs.corun_time ? 8 : 0) +
                                            (h_pairs.corun_chosen ? 1 : 0) + (h_pairs.weight ? 8 : 0));
-    CopyLane *lane = (nb == 1 && d2h_bytes >= min_chunk_bytes && mapped_v(h_weights) &&
+    CopyLane *lane = (d2h_bytes >= min_chunk_bytes && mapped_v(h_weights) &&
                       (!h_pairs.corun_grid_index || mapped_v(h_pairs.corun_grid_index)) &&
                       (!h_pairs.corun_time || mapped_v(h_pairs.corun_time)) &&
                       (!h_pairs.corun_chosen || mapped_v(h_pairs.corun_chosen)) &&
@@ -2242,9 +2242,13 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
                 CS_TRY(cudaMemsetAsync(&dcnt->queue_len, 0, sizeof(uint32_t), st));
                 CS_TRY(cudaMemsetAsync(&dcnt->exact_rows, 0, sizeof(uint32_t), st));
             }
+            // a chunk's records sit budget-major inside its own slice of the
+            // workspace arrays, [nb p0, nb p1): the kernels index them with
+            // the chunk's pair count as the budget stride
+            const size_t np = (size_t)(p1 - p0), q0 = (size_t)nb * (size_t)p0;
             if (p1 > p0) {
-                cs_pair_out pk{po.corun_grid_index + p0, po.corun_time + p0, po.corun_chosen + p0,
-                               po.weight + p0};
+                cs_pair_out pk{po.corun_grid_index + q0, po.corun_time + q0, po.corun_chosen + q0,
+                               po.weight + q0};
                 CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
                                           so.solo_clamps, p0, p1, rel_eps, pk, (int64_t *)(ws + L.queue),
                                           dcnt, (unsigned long long *)(ws + L.clamps),
@@ -2257,20 +2261,22 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
             // min(a, b) in [r0, r1)) -- the columns left of r0 went with
             // earlier chunks, so the copy after the last chunk is only its
             // diagonal block
-            const double *dW = (const double *)(ws + L.W);
-            CS_TRY(cudaMemcpy2DAsync(h_weights + r0 * n + r0, sizeof(double) * n, dW + r0 * n + r0,
-                                     sizeof(double) * n, sizeof(double) * (n - r0), (size_t)(r1 - r0),
-                                     cudaMemcpyDeviceToHost, lane->s));
-            if ((size_t)r1 < n)
-                CS_TRY(cudaMemcpy2DAsync(h_weights + r1 * n + r0, sizeof(double) * n, dW + r1 * n + r0,
-                                         sizeof(double) * n, sizeof(double) * (r1 - r0), n - (size_t)r1,
+            for (int l = 0; l < nb; ++l) {
+                const double *dW = (const double *)(ws + L.W) + (size_t)l * n * n;
+                double *hW = h_weights + (size_t)l * n * n;
+                CS_TRY(cudaMemcpy2DAsync(hW + r0 * n + r0, sizeof(double) * n, dW + r0 * n + r0,
+                                         sizeof(double) * n, sizeof(double) * (n - r0), (size_t)(r1 - r0),
                                          cudaMemcpyDeviceToHost, lane->s));
-            const size_t np = (size_t)(p1 - p0);
-            if (np) {
-                if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index + p0, po.corun_grid_index + p0, 4 * np, cudaMemcpyDeviceToHost, lane->s));
-                if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time + p0, po.corun_time + p0, 8 * np, cudaMemcpyDeviceToHost, lane->s));
-                if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen + p0, po.corun_chosen + p0, np, cudaMemcpyDeviceToHost, lane->s));
-                if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight + p0, po.weight + p0, 8 * np, cudaMemcpyDeviceToHost, lane->s));
+                if ((size_t)r1 < n)
+                    CS_TRY(cudaMemcpy2DAsync(hW + r1 * n + r0, sizeof(double) * n, dW + r1 * n + r0,
+                                             sizeof(double) * n, sizeof(double) * (r1 - r0), n - (size_t)r1,
+                                             cudaMemcpyDeviceToHost, lane->s));
+                if (!np) continue;
+                const size_t src = q0 + (size_t)l * np, dst = (size_t)l * (size_t)P + (size_t)p0;
+                if (h_pairs.corun_grid_index) CS_TRY(cudaMemcpyAsync(h_pairs.corun_grid_index + dst, po.corun_grid_index + src, 4 * np, cudaMemcpyDeviceToHost, lane->s));
+                if (h_pairs.corun_time) CS_TRY(cudaMemcpyAsync(h_pairs.corun_time + dst, po.corun_time + src, 8 * np, cudaMemcpyDeviceToHost, lane->s));
+                if (h_pairs.corun_chosen) CS_TRY(cudaMemcpyAsync(h_pairs.corun_chosen + dst, po.corun_chosen + src, np, cudaMemcpyDeviceToHost, lane->s));
+                if (h_pairs.weight) CS_TRY(cudaMemcpyAsync(h_pairs.weight + dst, po.weight + src, 8 * np, cudaMemcpyDeviceToHost, lane->s));
             }
         }
         CS_TRY(cudaEventRecord(lane->ev[K], lane->s));     // join the copies back

@@ -244,3 +244,32 @@ def test_zero_copy_epilogue_with_misaligned_pinned_outputs(weights):
             assert np.array_equal(st, ref["solo_time"][0])
     finally:
         lib.cs_workspace_release(ws_ptr)
+
+
+def test_chunked_host_call_with_two_budgets(weights):
+    """Two budgets, ~17 MB of pinned outputs: the row-chunked call keeps each
+    chunk's records budget-major in its own workspace slice and copies them to
+    their places in the L x P host arrays; every budget equals the oracle."""
+    from paper_2405_03831_b200.host_abi import HostGraphCall
+    n = 760
+    F, T = workload(n, 13)
+    grid = KnobGrid([core.default_space(400.0), core.default_space(350.0)])
+    ref = oracle.sweep(weights, F, T, grid)
+    iu, ju = np.triu_indices(n, 1)
+    call = HostGraphCall(weights, grid, n, with_records=True)
+    try:
+        for _ in range(3):
+            call.h_weights[...] = -1.0
+            call.h_idx[...] = -7
+            out = call(F, T)
+            for l in range(2):
+                W = out["weights"][l]
+                assert np.array_equal(W[iu, ju], ref["weight"][l])
+                assert np.array_equal(W[ju, iu], ref["weight"][l])
+                assert np.array_equal(call.h_idx[l], ref["corun_grid_index"][l])
+                assert np.array_equal(call.h_ct[l], ref["corun_time"][l])
+                assert np.array_equal(call.h_ch[l].astype(bool), ref["corun_chosen"][l])
+                assert np.array_equal(call.h_solo_time[l], ref["solo_time"][l])
+            assert int(call.h_clamps[0]) >= 0
+    finally:
+        call.close()
