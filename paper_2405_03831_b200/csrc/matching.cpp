@@ -31,6 +31,9 @@
 #include <cstdint>
 #include <cstring>
 #include <vector>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -845,6 +848,15 @@ std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, Row
 // the reference's verify-optimum condition on all n(n-1)/2 edges).
 int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, RowPool &pool) {
     const int n = f.n;
+    static const bool dbg = getenv("CM_DEBUG") != nullptr;
+    auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t_mark = now();
+    auto lap = [&](const char *what, long long x) {
+        if (!dbg) return;
+        const double t = now();
+        fprintf(stderr, "cm: %-22s %8.1f ms  (%lld)\n", what, 1e3 * (t - t_mark), x);
+        t_mark = t;
+    };
     if (k <= 0 || k >= n - 1) k = n - 1;
     int extra = 1;
     auto W = [&](int u, int v) { return scaled(f(u, v), shift) << extra; };
@@ -892,6 +904,7 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
             dd[u] = (double)dual[u];
         });
     }
+    lap("auction + duals", n);
     // ---- 3. candidates by slack (double: a heuristic), jump start, backbone ----
     std::vector<std::vector<int>> cand(n);
     pool.run(n, [&](int u, int) {
@@ -961,11 +974,17 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
     }
     Graph g = make_graph(f, edges, shift);
     int extra0 = extra;
+    {
+        long long free0 = 0;
+        for (int v = 0; v < n; ++v) free0 += mate[v] < 0;
+        lap("candidates + jump", free0);
+    }
 
     for (int round = 0; round < 64; ++round) {
         Blossom m(g);
         m.warm(dual, mate, extra);
         m.run(true);
+        lap("blossom run", (long long)edges.size());
         extra = m.extra();
         const std::vector<i128> &bd = m.duals();
         const std::vector<int> &parent = m.parents();
@@ -1009,6 +1028,26 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
         });
         size_t nbad = 0;
         for (int i = 0; i < n; ++i) nbad += bad[i].size();
+        if (dbg) {
+            long long zero = 0, single = 0;
+            for (int i = 0; i < n; ++i) {
+                if (mm[i] < 0) single += (long long)bad[i].size();
+                for (auto &x : bad[i]) zero += f(i, x.second) == 0.0;
+            }
+            long long nblos = 0;
+            for (int v = 0; v < n; ++v) nblos += parent[v] >= 0;
+            long double val = 0;
+            long long negd = 0;
+            for (int v = 0; v < n; ++v) {
+                if (mm[v] > v) val += f(v, mm[v]);
+                i128 y = bd[v];
+                for (int b = parent[v]; b >= 0; b = parent[b]) y += bd[b];
+                negd += y < 0;
+            }
+            fprintf(stderr, "cm:   violators on zero-value edges %lld, of unmatched rows %lld; vertices in blossoms %lld;"
+                    " matching value %.12Lf; negative flattened duals %lld\n", zero, single, nblos, val, negd);
+        }
+        lap("certificate", (long long)nbad);
         if (nbad == 0) {
             for (int v = 0; v < n; ++v) mate_out[v] = mm[v];
             return 0;
