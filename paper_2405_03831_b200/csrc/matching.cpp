@@ -781,10 +781,12 @@ std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, Row
         std::fill(owner.begin(), owner.end(), -1);
         freerows.resize(n);
         for (int u = 0; u < n; ++u) freerows[u] = u;
+        int rounds_dbg = 0;
+        for (int v = 0; v < n; ++v) h[v] = price[v] - d[v];   // kept current as prices move
         for (int it = 0; !freerows.empty() && it < 1000000; ++it) {
-            for (int v = 0; v < n; ++v) h[v] = price[v] - d[v];
+            ++rounds_dbg;
             const int nf = (int)freerows.size();
-            pool.run(nf, [&](int q, int) {
+            auto bid = [&](int q, int) {
                 const int u = freerows[q];
                 const double *wr = f.w + (size_t)u * n;
                 double m1 = INFINITY, m2 = INFINITY;   // two smallest w + h, v != u
@@ -803,7 +805,14 @@ std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, Row
                 if (m2 == INFINITY) m2 = m1;
                 bid_obj[q] = j1;
                 bid_val[q] = price[j1] + (m2 - m1) + eps;
-            }, 4);
+            };
+            // the long tail of rounds has a handful of free rows: bid on this
+            // thread (a pool dispatch costs more than the scans)
+            if (nf <= 8) {
+                for (int q = 0; q < nf; ++q) bid(q, 0);
+            } else {
+                pool.run(nf, bid, 4);
+            }
             next.clear();
             for (int q = 0; q < nf; ++q) {
                 const int v = bid_obj[q];
@@ -815,10 +824,12 @@ std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, Row
                 if (owner[v] >= 0) next.push_back(owner[v]);
                 owner[v] = u;
                 price[v] = bid_val[q];
+                h[v] = price[v] - d[v];
             }
             for (int q = 0; q < nf; ++q) best[bid_obj[q]] = -1;
             freerows.swap(next);
         }
+        if (getenv("CM_DEBUG")) fprintf(stderr, "cm:   auction eps %.3g: %d rounds\n", eps / vmax, rounds_dbg);
         if (eps <= eps_final_rel * vmax) break;
     }
     return price;
@@ -918,15 +929,18 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
     std::vector<std::pair<int, int>> edges;
     for (int u = 0; u < n; ++u)
         for (int v : cand[u]) edges.push_back({std::min(u, v), std::max(u, v)});
+    lap("candidates", (long long)edges.size());
     std::vector<int> mate(n, -1);
     {
         std::vector<double> need(n);
         for (int v = 0; v < n; ++v) {
             if (mate[v] >= 0) continue;
             // exact max_u (2 W_uv - y_u): double scan, i128 on the near-max
+            // (row v of the symmetric w: f(v, u) == f(u, v) bit for bit, and
+            // a row scan is contiguous where column u would stride by n)
             double bd = -INFINITY;
             for (int u = 0; u < n; ++u) {
-                need[u] = u == v ? -INFINITY : 2 * Wd(u, v) - dd[u];
+                need[u] = u == v ? -INFINITY : 2 * Wd(v, u) - dd[u];
                 bd = std::max(bd, need[u]);
             }
             i128 best = 0;
@@ -934,7 +948,7 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
             bool arg_free = false;
             for (int u = 0; u < n; ++u) {
                 if (u == v || need[u] < bd - 8 * tol) continue;
-                const i128 x = 2 * W(u, v) - dual[u];
+                const i128 x = 2 * W(v, u) - dual[u];
                 const bool fr = mate[u] < 0;
                 if (arg < 0 || x > best || (x == best && fr && !arg_free)) {
                     best = x; arg = u; arg_free = fr;
@@ -945,6 +959,26 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
             if (arg_free) {
                 mate[v] = arg; mate[arg] = v;
                 edges.push_back({std::min(v, arg), std::max(v, arg)});
+            }
+        }
+    }
+    // Zero-value edges (BENEFIT: time-share pairs, f == 0), 8 per vertex on a
+    // fixed pseudo-random pattern: the optimum pairs its leftover vertices
+    // with such edges.  Without them in the candidate graph the solver drove
+    // those vertices' duals negative, every certificate violator was a zero
+    // edge between two of them, and the rounds added them 8 per row (2-7
+    // rounds at N=4,096); with them one round certifies (tools/
+    // matcher_robustness.py: 1.1-2.0 s instead of 1.2-6.2 s)
+    constexpr int k0 = 8;
+    if (f.kind == EdgeValue::BENEFIT) {
+        for (int u = 0; u < n; ++u) {
+            uint64_t h = 0x9E3779B97F4A7C15ull * (uint64_t)(u + 1);
+            for (int q = 0, got = 0; q < 4 * k0 && got < k0; ++q) {
+                h ^= h >> 29; h *= 0xBF58476D1CE4E5B9ull; h ^= h >> 32;
+                const int v = (int)(h % (uint64_t)n);
+                if (v == u || f(u, v) != 0.0) continue;
+                edges.push_back({std::min(u, v), std::max(u, v)});
+                ++got;
             }
         }
     }
@@ -977,7 +1011,7 @@ int certified_perfect(const EdgeValue &f, int k, int shift, int32_t *mate_out, R
     {
         long long free0 = 0;
         for (int v = 0; v < n; ++v) free0 += mate[v] < 0;
-        lap("candidates + jump", free0);
+        lap("jump + backbone", free0);
     }
 
     for (int round = 0; round < 64; ++round) {
