@@ -782,10 +782,12 @@ std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, Row
         freerows.resize(n);
         for (int u = 0; u < n; ++u) freerows[u] = u;
         int rounds_dbg = 0;
+        long long bids_dbg = 0;
         for (int v = 0; v < n; ++v) h[v] = price[v] - d[v];   // kept current as prices move
         for (int it = 0; !freerows.empty() && it < 1000000; ++it) {
             ++rounds_dbg;
             const int nf = (int)freerows.size();
+            bids_dbg += nf;
             auto bid = [&](int q, int) {
                 const int u = freerows[q];
                 const double *wr = f.w + (size_t)u * n;
@@ -829,7 +831,8 @@ std::vector<double> auction_prices(const EdgeValue &f, double eps_final_rel, Row
             for (int q = 0; q < nf; ++q) best[bid_obj[q]] = -1;
             freerows.swap(next);
         }
-        if (getenv("CM_DEBUG")) fprintf(stderr, "cm:   auction eps %.3g: %d rounds\n", eps / vmax, rounds_dbg);
+        if (getenv("CM_DEBUG"))
+            fprintf(stderr, "cm:   auction eps %.3g: %d rounds, %lld bids\n", eps / vmax, rounds_dbg, bids_dbg);
         if (eps <= eps_final_rel * vmax) break;
     }
     return price;
