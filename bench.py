@@ -723,7 +723,7 @@ def run_multi(args, name, world, rank, local_rank, dev, weights):
     step_ms, sweep_ms = [], []
     dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev.index or 0) as clk:
         t_wall = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
