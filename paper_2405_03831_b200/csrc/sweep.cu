@@ -1845,10 +1845,9 @@ struct CallEndArgs {
     uint32_t aligned;                 // bit g: segment g's src and dst are 16-byte aligned
     int n;
 };
-__global__ void k_call_end(const CallEndArgs a) {
+__device__ __forceinline__ void copy_segments(const CallEndArgs &a, int64_t k0, int64_t stride) {
     const int64_t total = a.start16[a.n];
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
-         k += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t k = k0; k < total; k += stride) {
         int g = 0;
         while (k >= a.start16[g + 1]) ++g;
         const int64_t off = (k - a.start16[g]) * 16;
@@ -1861,6 +1860,51 @@ __global__ void k_call_end(const CallEndArgs a) {
             for (int b = 0; b < m; ++b) a.dst[g][off + b] = a.src[g][off + b];
         }
     }
+}
+__global__ void k_call_end(const CallEndArgs a) {
+    copy_segments(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// After a bulk copy of the matrix and records that ran concurrently with
+// k_resolve: re-copy what k_resolve may have changed -- the records and the
+// two matrix entries of every resolved (pair, budget) -- then the small
+// outputs.  Stream order puts these writes after the bulk copy's.
+struct CallFixArgs {
+    CallEndArgs small;
+    const int64_t *queue;
+    const cs_counters *cnt;
+    cs_pair_out dev, host;            // host: device-visible pinned pointers (null: not requested)
+    const double *W;
+    double *hW;                       // null: no matrix requested
+    int64_t P;
+    int n;
+};
+__global__ void k_call_fixup(const CallFixArgs a) {
+    const int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    const uint32_t q = a.cnt->queue_len;
+    for (int64_t k = k0; k < q; k += stride) {
+        const int64_t e = a.queue[k];
+        if (e & 8) continue;          // sampled re-scans of certain winners change nothing
+        const int64_t pl = e >> 4;
+        const int l = (int)(e & 7);
+        const int64_t o = (int64_t)l * a.P + pl;
+        // bytewise: the caller's host arrays need not be aligned
+        auto put = [](void *dst, const void *src, int bytes) {
+            for (int b = 0; b < bytes; ++b) ((uint8_t *)dst)[b] = ((const uint8_t *)src)[b];
+        };
+        if (a.host.corun_grid_index) put(a.host.corun_grid_index + o, a.dev.corun_grid_index + o, 4);
+        if (a.host.corun_time) put(a.host.corun_time + o, a.dev.corun_time + o, 8);
+        if (a.host.corun_chosen) put(a.host.corun_chosen + o, a.dev.corun_chosen + o, 1);
+        if (a.host.weight) put(a.host.weight + o, a.dev.weight + o, 8);
+        if (a.hW) {
+            int i, j;
+            pair_of(pl, a.n, i, j);
+            const size_t b = (size_t)l * a.n * a.n;
+            put(a.hW + b + (size_t)i * a.n + j, a.W + b + (size_t)i * a.n + j, 8);
+            put(a.hW + b + (size_t)j * a.n + i, a.W + b + (size_t)j * a.n + i, 8);
+        }
+    }
+    copy_segments(a.small, k0, stride);
 }
 
 // device-visible address of a pinned host buffer, or null (pageable / unknown)
@@ -2212,12 +2256,17 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     const double d2h_bytes = (h_weights ? 8.0 * n * n * nb : 0.0) +
                              (double)LP * ((h_pairs.corun_grid_index ? 4 : 0) + (h_pairs.corun_time ? 8 : 0) +
                                            (h_pairs.corun_chosen ? 1 : 0) + (h_pairs.weight ? 8 : 0));
-    CopyLane *lane = (d2h_bytes >= min_chunk_bytes && mapped_v(h_weights) &&
-                      (!h_pairs.corun_grid_index || mapped_v(h_pairs.corun_grid_index)) &&
-                      (!h_pairs.corun_time || mapped_v(h_pairs.corun_time)) &&
-                      (!h_pairs.corun_chosen || mapped_v(h_pairs.corun_chosen)) &&
-                      (!h_pairs.weight || mapped_v(h_pairs.weight)))
-                         ? copy_lane() : nullptr;
+    const bool big_mapped = (!h_weights || mapped_v(h_weights)) &&
+                            (!h_pairs.corun_grid_index || mapped_v(h_pairs.corun_grid_index)) &&
+                            (!h_pairs.corun_time || mapped_v(h_pairs.corun_time)) &&
+                            (!h_pairs.corun_chosen || mapped_v(h_pairs.corun_chosen)) &&
+                            (!h_pairs.weight || mapped_v(h_pairs.weight));
+    const bool all_mapped = big_mapped && (!h_solo.solo_time || mapped_v(h_solo.solo_time)) &&
+                            (!h_solo.solo_split || mapped_v(h_solo.solo_split)) &&
+                            (!h_solo.solo_clamps || mapped_v(h_solo.solo_clamps)) &&
+                            (!h_clamps || mapped_v(h_clamps)) && h_counters && mapped_v(h_counters);
+    CopyLane *lane = (d2h_bytes >= min_chunk_bytes && h_weights && big_mapped) ? copy_lane() : nullptr;
+    CopyLane *fork = nullptr;     // the small-graph path's second stream (below)
     if (lane) {
         const int K = 8;
         int64_t rows[K + 1];
@@ -2281,6 +2330,43 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
         }
         CS_TRY(cudaEventRecord(lane->ev[K], lane->s));     // join the copies back
         CS_TRY(cudaStreamWaitEvent(st, lane->ev[K], 0));
+    } else if (fp16_screen_safe(net) && all_mapped && (fork = copy_lane()) != nullptr) {
+        // the screen, then the bulk copy of the matrix and records on a second
+        // stream WHILE k_resolve re-scans the few queued pairs; k_call_fixup
+        // (below) re-copies those pairs once both are done
+        double *dW = h_weights ? (double *)(ws + L.W) : nullptr;
+        CS_RC(cs_pair_screen_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
+                                   so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue), dcnt,
+                                   (unsigned long long *)(ws + L.clamps), dW, CS_KERNEL_TCGEN05, stream));
+        CS_TRY(cudaEventRecord(fork->ev[0], st));
+        CS_TRY(cudaStreamWaitEvent(fork->s, fork->ev[0], 0));
+        CallEndArgs bulk{};
+        auto add = [&bulk](void *h_dst, const void *d_src, size_t bytes) {
+            if (!h_dst || !bytes) return;
+            void *m = mapped_v(h_dst);
+            bulk.src[bulk.n] = (const uint8_t *)d_src;
+            bulk.dst[bulk.n] = (uint8_t *)m;
+            bulk.bytes[bulk.n] = (int64_t)bytes;
+            if ((((uintptr_t)d_src | (uintptr_t)m) & 15) == 0) bulk.aligned |= 1u << bulk.n;
+            bulk.start16[bulk.n + 1] = bulk.start16[bulk.n] + (int64_t)((bytes + 15) / 16);
+            ++bulk.n;
+        };
+        if (h_weights) add(h_weights, ws + L.W, sizeof(double) * n * n * nb);
+        add(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP);
+        add(h_pairs.corun_time, po.corun_time, 8 * LP);
+        add(h_pairs.corun_chosen, po.corun_chosen, LP);
+        add(h_pairs.weight, po.weight, 8 * LP);
+        if (bulk.n) {
+            int blocks = (int)((bulk.start16[bulk.n] + 255) / 256);
+            if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
+            k_call_end<<<blocks, 256, 0, fork->s>>>(bulk);
+            CS_TRY(cudaGetLastError());
+        }
+        CS_TRY(cudaEventRecord(fork->ev[1], fork->s));
+        CS_RC(cs_resolve_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time, so.solo_clamps,
+                               0, P, po, (int64_t *)(ws + L.queue), dcnt, (unsigned long long *)(ws + L.clamps),
+                               dW, stream));
+        CS_TRY(cudaStreamWaitEvent(st, fork->ev[1], 0));
     } else {
         CS_RC(cs_pair_sweep_fused(net, &t, &dg, (const double *)(ws + L.bt), so.solo_time,
                                   so.solo_clamps, 0, P, rel_eps, po, (int64_t *)(ws + L.queue), dcnt,
@@ -2303,7 +2389,7 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
         e.start16[e.n + 1] = e.start16[e.n] + (int64_t)((bytes + 15) / 16);
         ++e.n;
     };
-    if (!lane) {
+    if (!lane && !fork) {
         if (h_weights) seg(h_weights, ws + L.W, sizeof(double) * n * n * nb);
         seg(h_pairs.corun_grid_index, po.corun_grid_index, 4 * LP);
         seg(h_pairs.corun_time, po.corun_time, 8 * LP);
@@ -2315,7 +2401,21 @@ int enqueue_graph_call(const cs_network *net, const cs_grid *h_grid, const doubl
     seg(h_solo.solo_clamps, so.solo_clamps, 4 * LN);
     seg(h_clamps, ws + L.clamps, 8 * (size_t)nb);
     seg(h_counters, ws + L.qcount, sizeof(cs_counters));
-    if (zc_out) {
+    if (fork) {
+        CallFixArgs fx{};
+        fx.small = e;
+        fx.queue = (const int64_t *)(ws + L.queue);
+        fx.cnt = dcnt;
+        fx.dev = po;
+        fx.host = cs_pair_out{(int32_t *)mapped_v(h_pairs.corun_grid_index), (double *)mapped_v(h_pairs.corun_time),
+                              (uint8_t *)mapped_v(h_pairs.corun_chosen), (double *)mapped_v(h_pairs.weight)};
+        fx.W = (const double *)(ws + L.W);
+        fx.hW = h_weights ? (double *)mapped_v(h_weights) : nullptr;
+        fx.P = P;
+        fx.n = n_apps;
+        k_call_fixup<<<sm_count(), 256, 0, st>>>(fx);
+        CS_TRY(cudaGetLastError());
+    } else if (zc_out) {
         const int64_t items = e.start16[e.n];
         int blocks = (int)((items + 255) / 256);
         if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
