@@ -147,15 +147,17 @@ __device__ double chunk_grads(Smem &s, int nc, double two_over_n) {
 
 // Gradient and loss of one batch of n rows, chunk by chunk; result in s.G and
 // s.loss (all threads see it after the final barrier).
+// `staged`: the batch (n <= kChunk) already sits in s.X / s.t
 template <class RowOf>
-__device__ void batch_grads(Smem &s, const double *x, const double *t, RowOf rows_of, int n) {
+__device__ void batch_grads(Smem &s, const double *x, const double *t, RowOf rows_of, int n,
+                            bool staged = false) {
     for (int i = threadIdx.x; i < NP; i += blockDim.x) s.G[i] = 0.0;
     __syncthreads();
     const double two_over_n = __ddiv_rn(2.0, (double)n);
     double sq = 0.0;
     for (int c0 = 0; c0 < n; c0 += kChunk) {
         const int nc = n - c0 < kChunk ? n - c0 : kChunk;
-        load_chunk(s, x, t, rows_of, c0, nc);
+        if (!staged) load_chunk(s, x, t, rows_of, c0, nc);
         sq = __dadd_rn(sq, chunk_grads(s, nc, two_over_n));
     }
     if (threadIdx.x == 0) s.loss = __ddiv_rn(sq, (double)n);
@@ -194,10 +196,40 @@ __global__ void __launch_bounds__(kThreads) k_train(const TrainArgs a) {
     for (int e = 0; e < a.epochs; ++e) {
         const int32_t *order = a.order + ((size_t)r * a.epochs + e) * a.n_train;
         double *bl = a.batch_loss + ((size_t)r * a.epochs + e) * a.nb;
+        // Small batches (all of a batch's elements fit one per thread): the
+        // next batch's rows are fetched into registers at the start of a step
+        // and staged after its update, so the order -> row -> x chain of
+        // dependent global loads leaves the step's critical path
+        const bool prefetch = a.batch * (IN + 1) <= (int)blockDim.x;
+        const int tid = threadIdx.x;
+        auto fetch = [&](int q, double &v) {
+            const int s0 = q * a.batch;
+            const int n = a.n_train - s0 < a.batch ? a.n_train - s0 : a.batch;
+            if (tid < n * IN) {
+                const int b = tid / IN, k = tid - b * IN;
+                v = __ldg(a.x + (size_t)train_rows[order[s0 + b]] * IN + k);
+            } else if (tid < n * IN + n) {
+                v = __ldg(a.t + train_rows[order[s0 + tid - n * IN]]);
+            }
+        };
+        auto stage = [&](int q, double v) {
+            const int s0 = q * a.batch;
+            const int n = a.n_train - s0 < a.batch ? a.n_train - s0 : a.batch;
+            if (tid < n * IN) s.X[tid] = v;
+            else if (tid < n * IN + n) s.t[tid - n * IN] = v;
+        };
+        if (prefetch) {
+            double v0 = 0.0;
+            fetch(0, v0);
+            stage(0, v0);
+            __syncthreads();
+        }
         for (int q = 0; q < a.nb; ++q) {
             const int s0 = q * a.batch;
             const int n = a.n_train - s0 < a.batch ? a.n_train - s0 : a.batch;
-            batch_grads(s, a.x, a.t, [&](int b) { return train_rows[order[s0 + b]]; }, n);
+            double next = 0.0;
+            if (prefetch && q + 1 < a.nb) fetch(q + 1, next);
+            batch_grads(s, a.x, a.t, [&](int b) { return train_rows[order[s0 + b]]; }, n, prefetch);
             const double loss = s.loss;
             if (!isfinite(loss)) {                 // fnn.py:288-289: TrainingDivergedError(epoch)
                 if (threadIdx.x == 0) a.status[r] = e;
@@ -206,6 +238,7 @@ __global__ void __launch_bounds__(kThreads) k_train(const TrainArgs a) {
             if (threadIdx.x == 0) bl[q] = loss;
             for (int i = threadIdx.x; i < NP; i += blockDim.x)
                 s.P[i] = __dsub_rn(s.P[i], __dmul_rn(a.lr, s.G[i]));   // sgd_step
+            if (prefetch && q + 1 < a.nb) stage(q + 1, next);       // s.X / s.t are free now
             __syncthreads();
         }
         // validation MSE after the epoch (fnn._mse): squared errors per row
