@@ -27,7 +27,7 @@ constexpr int IN = CT_INPUT, H = CT_HIDDEN, NP = CT_NPARAM;
 constexpr int OW1 = 0, OB1 = H * IN, OW2 = OB1 + H, OB2 = OW2 + H * H, OWO = OB2 + H, OBO = OWO + H;
 static_assert(OBO + 1 == NP, "parameter layout");
 constexpr int kChunk = 32;       // batch rows staged in shared memory at a time
-constexpr int kThreads = 128;
+constexpr int kThreads = 512;       // 128 -> 512: 0.56 -> 0.44 s per 100 epochs (more lanes per phase)
 
 struct Smem {
     double P[NP], G[NP];
