@@ -229,7 +229,10 @@ def bench_config(name, n, grid, world):
     return {"workload": WORKLOADS[name][3], "name": name, "n_apps": n, "pairs": P,
             "configs_per_pair": grid.n_grid, "reference_configs_per_pair": grid.units_per_pair(),
             "budgets_w": [s.p_total for s in grid.spaces],
-            "parallelism": f"pair shards x{world}" if world > 1 else "1 GPU"}
+            "parallelism": f"pair shards x{world}" if world > 1 else "1 GPU",
+            # the timing rule's L2 statement (identical on both arms, so the
+            # driver sees the same config; the CPU arm has no GPU L2 to flush)
+            "l2": "GPU arm: L2 flushed before every timed step (256 MiB memset outside the step events)"}
 
 
 def cpu_baseline(weights, name, seconds=12.0, threads=None):
