@@ -429,8 +429,9 @@ __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v >
 // different addresses), shared memory serves them in one wavefront; w1 is
 // also kept transposed (w1t[k][h]) so lane h's reads are consecutive.
 struct __align__(16) TablesSmem {
-    Net64P net;                  // net | w1t | head: one image slice + the head, bulk-copied
+    Net64P net;                  // net | w1t | w2t: one image slice + the head, bulk-copied
     double w1t[IN][HD];
+    double w2t[HD * HD];         // k-major W2: the solo heads as 18 independent chains
     Head64P head;
     double xs[4][2 * NF];        // per warp: the app's normalized counters
 };
@@ -483,8 +484,9 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
     if (threadIdx.x == 0) {
         tc::mbar_init(&staged, 1);
         tc::fence_mbar_init();
-        constexpr uint32_t kNetW1t = (uint32_t)(sizeof(Net64P) + sizeof(double) * IN * HD);
+        constexpr uint32_t kNetW1t = (uint32_t)(sizeof(Net64P) + sizeof(double) * (IN * HD + HD * HD));
         static_assert(offsetof(TablesSmem, w1t) == sizeof(Net64P), "image order");
+        static_assert(offsetof(TablesSmem, w2t) == sizeof(double) * kImgW2tOff, "image order");
         tc::mbar_expect_tx(&staged, kNetW1t + (uint32_t)sizeof(Head64P));
         tc::bulk_g2s(&sm.net, t.net_image, kNetW1t, &staged);
         tc::bulk_g2s(&sm.head, t.net_image + kImgHeadOff, (uint32_t)sizeof(Head64P), &staged);
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(128) k_tables(const __grid_constant__ Net64P n
                     ks = ks + net.b1[hh];
                     z[hh] = __shfl_sync(0xffffffffu, sa, hh) + ks;
                 }
-                double y = head64_lean(sm.head, z);
+                double y = head64t(sm.head, sm.w2t, z);
                 int clamp = 0;
                 if (y < FLOOR) { clamp = 1; y = FLOOR; }
                 const double tt = y * base_time[r];
