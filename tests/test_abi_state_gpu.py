@@ -273,3 +273,34 @@ def test_chunked_host_call_with_two_budgets(weights):
             assert int(call.h_clamps[0]) >= 0
     finally:
         call.close()
+
+
+def test_overlapped_small_call_two_budgets(weights):
+    """Below the chunking threshold with every destination pinned: the bulk
+    copy of matrix + records runs beside k_resolve and k_call_fixup re-copies
+    the resolved pairs.  Two budgets and a wide ambiguity band (rel_eps
+    2e-3: thousands of pairs go through k_resolve and the fixup); eager,
+    captured and replayed calls equal the oracle."""
+    from paper_2405_03831_b200.host_abi import HostGraphCall
+    n = 200
+    F, T = workload(n, 17)
+    grid = KnobGrid([core.default_space(400.0), core.default_space(375.0)])
+    ref = oracle.sweep(weights, F, T, grid)
+    iu, ju = np.triu_indices(n, 1)
+    call = HostGraphCall(weights, grid, n, with_records=True, rel_eps=2e-3)
+    try:
+        for _ in range(4):
+            call.h_weights[...] = -1.0
+            call.h_idx[...] = -7
+            call.h_ct[...] = 0.0
+            out = call(F, T)
+            for l in range(2):
+                W = out["weights"][l]
+                assert np.array_equal(W[iu, ju], ref["weight"][l])
+                assert np.array_equal(W[ju, iu], ref["weight"][l])
+                assert np.array_equal(call.h_idx[l], ref["corun_grid_index"][l])
+                assert np.array_equal(call.h_ct[l], ref["corun_time"][l])
+                assert np.array_equal(call.h_ch[l].astype(bool), ref["corun_chosen"][l])
+                assert np.array_equal(call.h_solo_split[l], ref["solo_split"][l])
+    finally:
+        call.close()
