@@ -6,7 +6,7 @@
 // r/2 of the group's 64-pair work item, member r%2) and one MMA-issuer warp
 // per group.  Per config the group's threads build their A rows (layer-1
 // ReLU, fp16 hi/lo split) straight into TMEM, the issuer warp's elected lane
-// issues 4 x tcgen05.mma M128 N32 K16 (A in TMEM, B = the W2 split in SMEM),
+// issues 4 x tcgen05.mma M128 N24 K16 (A in TMEM, B = the W2 split in SMEM),
 // and the epilogue reads D back with tcgen05.ld for the head and the argmin.
 // S = 2 TMEM stages pipeline build(c) against epilogue(c - 1).
 //
