@@ -677,14 +677,17 @@ public:
     ~RowPool() {
         {
             std::lock_guard<std::mutex> g(mu_);
-            stop_ = true;
-            ++gen_;
+            stop_.store(true);
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
         for (auto &t : th_) t.join();
     }
     int threads() const { return nt_; }
-    // body(i, thread) for i in [0, n); small loops run inline
+    // body(i, thread) for i in [0, n); small loops run inline.  Workers spin
+    // for a while after each job before they sleep: the auction dispatches
+    // tens of thousands of short rounds, and a futex wake-up per worker per
+    // round cost more than many rounds' work.
     template <class F>
     void run(int n, F &&body, int grain = 16) {
         if (nt_ == 1 || n < 2 * grain) {
@@ -692,26 +695,26 @@ public:
             return;
         }
         std::function<void(int, int)> fn = body;
+        job_ = &fn;
+        n_ = n;
+        grain_ = grain;
+        next_.store(0, std::memory_order_relaxed);
+        pending_.store(nt_ - 1, std::memory_order_relaxed);
         {
-            std::lock_guard<std::mutex> g(mu_);
-            job_ = &fn;
-            n_ = n;
-            grain_ = grain;
-            next_.store(0);
-            pending_ = nt_ - 1;
-            ++gen_;
+            std::lock_guard<std::mutex> g(mu_);      // pairs with a sleeper's predicate check
+            gen_.fetch_add(1, std::memory_order_release);
         }
-        cv_.notify_all();
+        if (sleepers_.load(std::memory_order_acquire) > 0) cv_.notify_all();
         chew(0);
-        std::unique_lock<std::mutex> g(mu_);
-        done_cv_.wait(g, [this] { return pending_ == 0; });
+        for (int spin = 0; pending_.load(std::memory_order_acquire) != 0; ++spin)
+            if (spin > 1024) std::this_thread::yield();
         job_ = nullptr;
     }
 
 private:
     void chew(int t) {
         for (;;) {
-            const int i0 = next_.fetch_add(grain_);
+            const int i0 = next_.fetch_add(grain_, std::memory_order_relaxed);
             if (i0 >= n_) break;
             const int i1 = std::min(n_, i0 + grain_);
             for (int i = i0; i < i1; ++i) (*job_)(i, t);
@@ -720,25 +723,33 @@ private:
     void worker(int t) {
         uint64_t seen = 0;
         for (;;) {
-            {
-                std::unique_lock<std::mutex> g(mu_);
-                cv_.wait(g, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (stop_) return;
+            // spin ~tens of microseconds for the next job, then sleep
+            bool got = false;
+            for (int spin = 0; spin < 20000; ++spin) {
+                if (gen_.load(std::memory_order_acquire) != seen) { got = true; break; }
+                if ((spin & 63) == 63) std::this_thread::yield();
             }
+            if (!got) {
+                std::unique_lock<std::mutex> g(mu_);
+                sleepers_.fetch_add(1, std::memory_order_acq_rel);
+                cv_.wait(g, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                sleepers_.fetch_sub(1, std::memory_order_acq_rel);
+            }
+            seen = gen_.load(std::memory_order_acquire);
+            if (stop_.load()) return;
             chew(t);
-            std::lock_guard<std::mutex> g(mu_);
-            if (--pending_ == 0) done_cv_.notify_one();
+            pending_.fetch_sub(1, std::memory_order_acq_rel);
         }
     }
     int nt_ = 1;
     std::vector<std::thread> th_;
     std::mutex mu_;
-    std::condition_variable cv_, done_cv_;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::condition_variable cv_;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<bool> stop_{false};
+    std::atomic<int> sleepers_{0}, pending_{0};
     std::function<void(int, int)> *job_ = nullptr;
-    int n_ = 0, grain_ = 16, pending_ = 0;
+    int n_ = 0, grain_ = 16;
     std::atomic<int> next_{0};
 };
 
