@@ -327,8 +327,10 @@ int cs_workspace_release(void *d_workspace);
  * (NULL members skipped); h_solo members: L x N host arrays (NULL skipped);
  * h_clamps: L (NULL to skip).  Full graph (all P pairs).  Synchronizes
  * `stream` before returning.  Transfers: pinned inputs are read by a
- * zero-copy kernel; when every destination is pinned, ONE epilogue kernel
- * writes all outputs into them over PCIe (else cudaMemcpyAsync per array);
+ * zero-copy kernel; when every destination is pinned, kernels write the
+ * outputs into them over PCIe -- the matrix and records on a second stream
+ * beside k_resolve, then a fixup of the resolved pairs and the small
+ * outputs (else cudaMemcpyAsync per array);
  * calls with >= 14 MB of pinned outputs sweep in 8 row chunks
  * and copy each finished row block while the next one computes. */
 int cs_build_graph_host(const cs_network *net, const cs_grid *h_grid, const double *h_features,
